@@ -1,0 +1,161 @@
+/*
+ * isinglink_b200 — C ABI of the B200-native MMGaP hot path.
+ *
+ * Drop-in boundary for the reference package `isinglink`
+ * (/root/reference/pkg/src/isinglink).  Every entry point below states the
+ * reference interface it replaces (file:line).  Conventions:
+ *   - plain pointers and sizes only; no torch / numpy types;
+ *   - functions named *_host take HOST pointers and are synchronous; all
+ *     others take DEVICE pointers and enqueue on `stream` (a cudaStream_t,
+ *     NULL = legacy default stream) without synchronising;
+ *   - complex arrays are interleaved (re, im) float64, i.e. numpy complex128
+ *     / torch.complex128 memory;
+ *   - return 0 (IL_OK) on success, a negative IL_ERR_* code otherwise, with a
+ *     human-readable message from il_last_error() (thread-local).  No C++
+ *     exception ever crosses the ABI.  Divergence of an anneal is data, not
+ *     an error (as in the reference).
+ */
+#ifndef ISINGLINK_B200_H
+#define ISINGLINK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IL_ABI_VERSION 1
+
+enum il_status {
+    IL_OK = 0,
+    IL_ERR_ARG = -1,         /* invalid argument (reference: ValueError/TypeError) */
+    IL_ERR_CUDA = -2,        /* CUDA runtime / launch failure */
+    IL_ERR_UNSUPPORTED = -3, /* shape/parameter combination not built */
+    IL_ERR_NOMEM = -4
+};
+
+/* Arithmetic of the anneal loop. */
+enum il_precision {
+    IL_PREC_FP64_EXACT = 0, /* FP64, reference evaluation order, no FMA contraction:
+                               bit-identical to the reference "ext" kernel */
+    IL_PREC_FP32 = 1,       /* FP32 state, coupling product on tensor cores with
+                               3xTF32 split (FP32-accurate); the throughput mode */
+    IL_PREC_TF32 = 2        /* FP32 state, single-pass TF32 coupling product */
+};
+
+/* Solver configuration — mirrors CacParams (solver.py:87-124). */
+typedef struct il_cac_params {
+    double p;                 /* gain                                  (1.5)  */
+    double a;                 /* target amplitude^2                    (0.5)  */
+    double zeta;              /* error-variable rate                   (1.0)  */
+    double eps;               /* coupling; <= 0 selects auto scaling   (auto) */
+    double dt;                /* Euler step                            (0.02) */
+    int32_t f_mvm;            /* coupling refresh period               (2)    */
+    int32_t n_steps;          /*                                       (128)  */
+    int32_t n_anneals;        /* replicas per problem                  (32)   */
+    int32_t precision;        /* il_precision                                 */
+    double diverge_threshold; /*                                       (10.0) */
+    double e_floor;           /*                                       (1e-6) */
+    double init_amplitude;    /*                                       (0.1)  */
+} il_cac_params;
+
+/* Per-problem outcome of a batched detection (DetectionResult, linear.py:33-41). */
+enum il_source { IL_SRC_GUESS = 0, IL_SRC_ANNEAL = 1, IL_SRC_FAILED = -1 };
+
+const char* il_last_error(void);
+int il_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Kernel plugin: replaces `_kernel.run_anneals` (_kernel.pyx:16-102, contract
+ * _kernel_py.py:24-92).  G[n_dim*n_dim], g_diag[n_dim], b[n_dim],
+ * x0[n_batch*(2*n_dim+1)] row-major float64.  Outputs: spins int8
+ * [n_batch*(2*n_dim+1)] with sign(0)=+1, diverged uint8[n_batch],
+ * steps int64[n_batch], mvms int64[n_batch].  Always FP64-exact.
+ * ------------------------------------------------------------------------- */
+int il_run_anneals(const double* G, const double* g_diag, const double* b,
+                   const double* x0, int32_t n_dim, int32_t n_batch, double dt,
+                   double p, double a, double zeta, double eps, double e_floor,
+                   int32_t f_mvm, int32_t n_steps, double diverge_threshold,
+                   int8_t* spins, uint8_t* diverged, int64_t* steps, int64_t* mvms,
+                   void* stream);
+int il_run_anneals_host(const double* G, const double* g_diag, const double* b,
+                        const double* x0, int32_t n_dim, int32_t n_batch, double dt,
+                        double p, double a, double zeta, double eps, double e_floor,
+                        int32_t f_mvm, int32_t n_steps, double diverge_threshold,
+                        int8_t* spins, uint8_t* diverged, int64_t* steps,
+                        int64_t* mvms);
+
+/* ---------------------------------------------------------------------------
+ * Seeds and initial states.
+ *   il_derive_seeds: out[i] = derive_seed(parts[i*n_parts + 0..n_parts))
+ *     (solver.py:137-144, numpy SeedSequence), n_parts <= 6.
+ *   il_initial_states: x0[i*S + k] = default_rng(seeds[i]).uniform(-amp, amp, S)[k]
+ *     (solver.py:182-187, numpy PCG64), bit-exact.
+ * ------------------------------------------------------------------------- */
+int il_derive_seeds(const uint64_t* parts, int32_t n_parts, int64_t n, uint64_t* out,
+                    void* stream);
+int il_initial_states(const uint64_t* seeds, int64_t n, int32_t S, double amplitude,
+                      double* x0, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Linear front-end + Ising reduction for P independent problems.
+ *   il_mmse_batch — detect_mmse (linear.py:55-75): hard MMSE decision as
+ *     level indices x_idx[P*n_t*2] (re, im) and residual energy[P].
+ *   il_build_ising_batch — build_ising (transform.py:108-140) around the
+ *     guess given as level indices of `levels` (qam_order > 0: unit-energy
+ *     QAM; qam_order < 0: VPP lattice of reach -qam_order).  Outputs
+ *     G[P*N*N], g_diag[P*N], b[P*N], offset[P], eps_scale[P] (N = 2*n_t).
+ * H is [P, n_r, n_t] complex128, y [P, n_r], noise_var [P].
+ * status[P] (optional, may be NULL): 0 ok, -1 Cholesky breakdown.
+ * ------------------------------------------------------------------------- */
+int il_mmse_batch(const double* H, const double* y, const double* noise_var,
+                  int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                  uint8_t* x_idx, double* energy, int8_t* status, void* stream);
+int il_build_ising_batch(const double* H, const double* y, const uint8_t* guess_idx,
+                         int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                         double* G, double* g_diag, double* b, double* offset,
+                         double* eps_scale, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batched uplink detection: P x detect_cim (detector.py:57-82) with
+ * seed[p] the `seed` argument of detect_cim for problem p.  Outputs:
+ *   x_idx[P*n_t*2] level indices (re, im) of x_hard,
+ *   energy[P] residual ||y - H x_hard||^2,
+ *   source[P] il_source, anneal_index[P] (-1 unless source == anneal),
+ *   diverged_count[P].
+ * Any output pointer except x_idx may be NULL.
+ * ------------------------------------------------------------------------- */
+int il_detect_cim_batch(const double* H, const double* y, const double* noise_var,
+                        int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                        const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
+                        double* energy, int8_t* source, int32_t* anneal_index,
+                        int32_t* diverged_count, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Batched downlink vector-perturbation precoding: P x precode_vpp
+ * (precoder.py:93-146).  H [P, n_u, n_ant] complex128 (n_u <= n_ant),
+ * u [P, n_u] complex128 symbols, power P_tot > 0, tau, n_stages >= 1,
+ * seed[p].  Outputs x[P*n_ant] complex128 transmit vector, v[P*n_u]
+ * complex128 perturbation (even Gaussian integers), unnorm_power[P],
+ * diverged_count[P] (may be NULL).
+ * ------------------------------------------------------------------------- */
+int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_u,
+                         int32_t n_ant, double power, double tau, int32_t n_stages,
+                         const uint64_t* seed, const il_cac_params* prm, double* x,
+                         double* v, double* unnorm_power, int32_t* diverged_count,
+                         void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Spin-to-bit demapper (channel.py:160-180 Gray labels).  For n_sym symbols
+ * with level indices x_idx[n_sym*2] (re, im) and bits_per_dim = log2(m):
+ * bits[n_sym * 2 * bits_per_dim] uint8 in {0,1}, ordered (re MSB..LSB,
+ * im MSB..LSB) per symbol.
+ * ------------------------------------------------------------------------- */
+int il_gray_demap(const uint8_t* x_idx, int64_t n_sym, int32_t bits_per_dim,
+                  uint8_t* bits, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ISINGLINK_B200_H */

@@ -1,0 +1,95 @@
+"""ctypes binding of the C ABI in include/isinglink_b200.h.
+
+The shared object is built in-tree by ``paper_2510_01579_b200.build``.  There
+is deliberately no fallback: if the library is missing or cannot be loaded,
+every entry point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libisinglink_b200.so")
+
+IL_OK, IL_ERR_ARG, IL_ERR_CUDA, IL_ERR_UNSUPPORTED, IL_ERR_NOMEM = 0, -1, -2, -3, -4
+PREC = {"fp64_exact": 0, "fp32": 1, "tf32": 2}
+
+_c_d = ctypes.c_double
+_c_i32 = ctypes.c_int32
+_c_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+
+class CacParamsC(ctypes.Structure):
+    """il_cac_params (field order must match the header)."""
+    _fields_ = [
+        ("p", _c_d), ("a", _c_d), ("zeta", _c_d), ("eps", _c_d), ("dt", _c_d),
+        ("f_mvm", _c_i32), ("n_steps", _c_i32), ("n_anneals", _c_i32), ("precision", _c_i32),
+        ("diverge_threshold", _c_d), ("e_floor", _c_d), ("init_amplitude", _c_d),
+    ]
+
+
+_SIGS = {
+    "il_last_error": ([], ctypes.c_char_p),
+    "il_abi_version": ([], ctypes.c_int),
+    "il_run_anneals": ([_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d,
+                        _c_i32, _c_i32, _c_d, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "il_run_anneals_host": ([_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_d, _c_d, _c_d, _c_d, _c_d,
+                             _c_d, _c_i32, _c_i32, _c_d, _vp, _vp, _vp, _vp], ctypes.c_int),
+    "il_derive_seeds": ([_vp, _c_i32, _c_i64, _vp, _vp], ctypes.c_int),
+    "il_initial_states": ([_vp, _c_i64, _c_i32, _c_d, _vp, _vp], ctypes.c_int),
+    "il_mmse_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp],
+                      ctypes.c_int),
+    "il_build_ising_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp,
+                              _vp, _vp], ctypes.c_int),
+    "il_detect_cim_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
+                             ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _vp],
+                            ctypes.c_int),
+    "il_precode_vpp_batch": ([_vp, _vp, _c_i64, _c_i32, _c_i32, _c_d, _c_d, _c_i32, _vp,
+                              ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp],
+                             ctypes.c_int),
+    "il_gray_demap": ([_vp, _c_i64, _c_i32, _vp, _vp], ctypes.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load (once) and return the CDLL with typed entry points."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(
+                    f"isinglink_b200 CUDA library not built ({path}); run "
+                    "`python -m paper_2510_01579_b200.build` (there is no CPU fallback)")
+            lib = ctypes.CDLL(path)
+            for name, (args, res) in _SIGS.items():
+                fn = getattr(lib, name)
+                fn.argtypes = args
+                fn.restype = res
+            _lib = lib
+    return _lib
+
+
+class IsinglinkError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def check(rc: int) -> None:
+    if rc != IL_OK:
+        msg = load().il_last_error().decode(errors="replace")
+        if rc == IL_ERR_ARG:
+            raise ValueError(msg)
+        raise IsinglinkError(rc, msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args))

@@ -1,0 +1,211 @@
+"""Batched device API: whole slots of resource elements per call.
+
+All functions take torch CUDA tensors (or numpy arrays, which are copied to
+the current device) and enqueue on the current torch stream; outputs are
+torch CUDA tensors.  Shapes use P = number of problems (resource elements):
+
+  H  complex128 [P, n_r, n_t]     y  complex128 [P, n_r]     noise_var f64 [P]
+  x_idx  uint8 [P, n_t, 2]        level indices (re, im) of the decided symbols
+
+These are the B200-native entry points the throughput benchmark drives; the
+reference-shaped per-instance API in ``api.py`` is built on them.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .params import CacParams, to_c
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _dev(x, dtype: torch.dtype) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x
+    else:
+        arr = np.ascontiguousarray(x)
+        t = torch.from_numpy(arr)
+    if t.device.type != "cuda":
+        t = t.to("cuda", non_blocking=False)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.contiguous()
+
+
+def _seeds(seeds, P: int) -> torch.Tensor:
+    if isinstance(seeds, torch.Tensor):
+        s = seeds
+    else:
+        s = torch.from_numpy(np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1)))
+    s = s.to("cuda").contiguous()
+    if s.dtype not in (torch.uint64, torch.int64):
+        raise TypeError("seeds must be uint64 (or int64 bit patterns)")
+    if s.numel() != P:
+        raise ValueError(f"expected {P} seeds, got {s.numel()}")
+    return s
+
+
+@dataclass
+class DetectBatch:
+    x_idx: torch.Tensor          # uint8 [P, n_t, 2]
+    energy: torch.Tensor         # f64 [P]   ||y - H x||^2
+    source: torch.Tensor         # int8 [P]  0 guess (MMSE), 1 anneal, -1 failed
+    anneal_index: torch.Tensor   # int32 [P] winning anneal or -1
+    diverged: torch.Tensor       # int32 [P] diverged anneal count
+
+
+def detect_cim_batch(H, y, noise_var, order: int, seeds, params=None,
+                     precision: str | None = None) -> DetectBatch:
+    """P x ``detect_cim`` (detector.py:57-82); seeds[p] is detect_cim's ``seed``."""
+    params = params or CacParams()
+    prm = to_c(params, precision)
+    Hd = _dev(H, torch.complex128)
+    if Hd.dim() != 3:
+        raise ValueError("H must be [P, n_r, n_t]")
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    sd = _dev(noise_var, torch.float64)
+    if yd.shape != (P, n_r) or sd.shape != (P,):
+        raise ValueError("y must be [P, n_r] and noise_var [P]")
+    seed_t = _seeds(seeds, P)
+    dev = Hd.device
+    out = DetectBatch(
+        x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8, device=dev),
+        energy=torch.empty(P, dtype=torch.float64, device=dev),
+        source=torch.empty(P, dtype=torch.int8, device=dev),
+        anneal_index=torch.empty(P, dtype=torch.int32, device=dev),
+        diverged=torch.empty(P, dtype=torch.int32, device=dev),
+    )
+    _lib.call("il_detect_cim_batch", Hd.data_ptr(), yd.data_ptr(), sd.data_ptr(), P, n_r, n_t,
+              int(order), seed_t.data_ptr(), prm, out.x_idx.data_ptr(), out.energy.data_ptr(),
+              out.source.data_ptr(), out.anneal_index.data_ptr(), out.diverged.data_ptr(),
+              _stream())
+    return out
+
+
+@dataclass
+class PrecodeBatch:
+    x: torch.Tensor              # complex128 [P, n_ant] power-normalised transmit vector
+    v: torch.Tensor              # complex128 [P, n_u] perturbation (even Gaussian integers)
+    unnormalized_power: torch.Tensor  # f64 [P]
+    diverged: torch.Tensor       # int32 [P]
+
+
+def precode_vpp_batch(H, u, power: float, tau: float, seeds, params=None, n_stages: int = 1,
+                      precision: str | None = None) -> PrecodeBatch:
+    """P x ``precode_vpp`` (precoder.py:93-146).  H [P, n_u, n_ant], u [P, n_u]."""
+    params = params or CacParams()
+    prm = to_c(params, precision)
+    Hd = _dev(H, torch.complex128)
+    P, n_u, n_ant = Hd.shape
+    ud = _dev(u, torch.complex128)
+    if ud.shape != (P, n_u):
+        raise ValueError("u must be [P, n_u]")
+    seed_t = _seeds(seeds, P)
+    dev = Hd.device
+    out = PrecodeBatch(
+        x=torch.empty((P, n_ant), dtype=torch.complex128, device=dev),
+        v=torch.empty((P, n_u), dtype=torch.complex128, device=dev),
+        unnormalized_power=torch.empty(P, dtype=torch.float64, device=dev),
+        diverged=torch.empty(P, dtype=torch.int32, device=dev),
+    )
+    _lib.call("il_precode_vpp_batch", Hd.data_ptr(), ud.data_ptr(), P, n_u, n_ant, float(power),
+              float(tau), int(n_stages), seed_t.data_ptr(), prm, out.x.data_ptr(),
+              out.v.data_ptr(), out.unnormalized_power.data_ptr(), out.diverged.data_ptr(),
+              _stream())
+    return out
+
+
+def mmse_batch(H, y, noise_var, order: int):
+    """P x ``detect_mmse`` (linear.py:55-75) -> (x_idx, energy, status)."""
+    Hd = _dev(H, torch.complex128)
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    sd = _dev(noise_var, torch.float64)
+    x_idx = torch.empty((P, n_t, 2), dtype=torch.uint8, device=Hd.device)
+    energy = torch.empty(P, dtype=torch.float64, device=Hd.device)
+    status = torch.empty(P, dtype=torch.int8, device=Hd.device)
+    _lib.call("il_mmse_batch", Hd.data_ptr(), yd.data_ptr(), sd.data_ptr(), P, n_r, n_t,
+              int(order), x_idx.data_ptr(), energy.data_ptr(), status.data_ptr(), _stream())
+    return x_idx, energy, status
+
+
+def build_ising_batch(H, y, guess_idx, order: int) -> dict:
+    """P x ``build_ising`` (transform.py:108-140) around level-index guesses.
+
+    order > 0: unit-energy QAM; order < 0: VPP lattice of reach -order."""
+    Hd = _dev(H, torch.complex128)
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    gd = _dev(guess_idx, torch.uint8)
+    N = 2 * n_t
+    dev = Hd.device
+    out = dict(G=torch.empty((P, N, N), dtype=torch.float64, device=dev),
+               g_diag=torch.empty((P, N), dtype=torch.float64, device=dev),
+               b=torch.empty((P, N), dtype=torch.float64, device=dev),
+               offset=torch.empty(P, dtype=torch.float64, device=dev),
+               eps_scale=torch.empty(P, dtype=torch.float64, device=dev))
+    _lib.call("il_build_ising_batch", Hd.data_ptr(), yd.data_ptr(), gd.data_ptr(), P, n_r, n_t,
+              int(order), out["G"].data_ptr(), out["g_diag"].data_ptr(), out["b"].data_ptr(),
+              out["offset"].data_ptr(), out["eps_scale"].data_ptr(), _stream())
+    return out
+
+
+def run_anneals(G, g_diag, b, x0, dt, p, a, zeta, eps, e_floor, f_mvm, n_steps,
+                diverge_threshold):
+    """Device-tensor form of the kernel plugin (FP64-exact, _kernel.pyx:16-102)."""
+    Gd = _dev(G, torch.float64)
+    gd = _dev(g_diag, torch.float64)
+    bd = _dev(b, torch.float64)
+    xd = _dev(x0, torch.float64)
+    nb, S = xd.shape
+    n = Gd.shape[0]
+    if S != 2 * n + 1:
+        raise ValueError("x0 must be (n_anneals, 2N+1)")
+    dev = xd.device
+    spins = torch.empty((nb, S), dtype=torch.int8, device=dev)
+    div = torch.empty(nb, dtype=torch.uint8, device=dev)
+    steps = torch.empty(nb, dtype=torch.int64, device=dev)
+    mvms = torch.empty(nb, dtype=torch.int64, device=dev)
+    _lib.call("il_run_anneals", Gd.data_ptr(), gd.data_ptr(), bd.data_ptr(), xd.data_ptr(), n, nb,
+              float(dt), float(p), float(a), float(zeta), float(eps), float(e_floor), int(f_mvm),
+              int(n_steps), float(diverge_threshold), spins.data_ptr(), div.data_ptr(),
+              steps.data_ptr(), mvms.data_ptr(), _stream())
+    return spins, div.bool(), steps, mvms
+
+
+def derive_seeds(parts) -> torch.Tensor:
+    """Row-wise ``derive_seed(*parts[i])`` (solver.py:137-144) on the device."""
+    arr = np.ascontiguousarray(np.asarray(parts, dtype=np.uint64))
+    if arr.ndim == 1:
+        arr = arr[:, None]
+    n, k = arr.shape
+    pd = torch.from_numpy(arr).to("cuda")
+    out = torch.empty(n, dtype=torch.uint64, device="cuda")
+    _lib.call("il_derive_seeds", pd.data_ptr(), k, n, out.data_ptr(), _stream())
+    return out
+
+
+def initial_states(seeds, S: int, amplitude: float) -> torch.Tensor:
+    """``default_rng(seed).uniform(-amp, amp, S)`` per seed (solver.py:182-187)."""
+    sd = _seeds(seeds, len(seeds) if not isinstance(seeds, torch.Tensor) else seeds.numel())
+    out = torch.empty((sd.numel(), S), dtype=torch.float64, device="cuda")
+    _lib.call("il_initial_states", sd.data_ptr(), sd.numel(), int(S), float(amplitude),
+              out.data_ptr(), _stream())
+    return out
+
+
+def gray_demap(x_idx, bits_per_dim: int) -> torch.Tensor:
+    """Level indices [..., 2] -> Gray bits [..., 2*bits_per_dim] (channel.py:160-180)."""
+    xd = _dev(x_idx, torch.uint8)
+    n_sym = xd.numel() // 2
+    out = torch.empty(xd.shape[:-1] + (2 * bits_per_dim,), dtype=torch.uint8, device=xd.device)
+    _lib.call("il_gray_demap", xd.data_ptr(), n_sym, int(bits_per_dim), out.data_ptr(), _stream())
+    return out

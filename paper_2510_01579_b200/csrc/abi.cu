@@ -1,0 +1,323 @@
+// extern "C" entry points (include/isinglink_b200.h) and the batched
+// pipelines that chain the kernels.  No C++ exception crosses this file's
+// boundary; every failure becomes an IL_ERR_* code plus il_last_error().
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "il_internal.cuh"
+#include "rng_numpy.cuh"
+
+namespace il {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+}
+
+int fail_cuda(cudaError_t e, const char* what) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return IL_ERR_CUDA;
+}
+
+Workspace::~Workspace() {
+    for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], st);
+}
+
+int make_qam_alphabet(int order, Alphabet* out) {
+    int m = 0;
+    switch (order) {
+        case 4: m = 2; break;
+        case 16: m = 4; break;
+        case 64: m = 8; break;
+        case 256: m = 16; break;
+        default:
+            set_error("unsupported QAM order %d; expected one of (4, 16, 64, 256)", order);
+            return IL_ERR_ARG;
+    }
+    // channel.py:88-108: odd integers / sqrt(2 (m^2 - 1) / 3)
+    const double norm = sqrt(2.0 * (double)(m * m - 1) / 3.0);
+    out->m = m;
+    out->spacing = 2.0 / norm;
+    for (int k = 0; k < m; ++k) out->levels[k] = (double)(-(m - 1) + 2 * k) / norm;
+    for (int k = 0; k + 1 < m; ++k) out->mids[k] = (out->levels[k] + out->levels[k + 1]) / 2.0;
+    return IL_OK;
+}
+
+int make_lattice_alphabet(int reach, Alphabet* out) {
+    // precoder.py:79-90: levels 4 * {-reach..reach}, spacing 4
+    if (reach < 1 || 2 * reach + 1 > 32) {
+        set_error("VPP n_stages must be in [1, 15], got %d", reach);
+        return IL_ERR_ARG;
+    }
+    out->m = 2 * reach + 1;
+    out->spacing = 4.0;
+    for (int k = 0; k < out->m; ++k) out->levels[k] = 4.0 * (double)(k - reach);
+    for (int k = 0; k + 1 < out->m; ++k) out->mids[k] = (out->levels[k] + out->levels[k + 1]) / 2.0;
+    return IL_OK;
+}
+
+static int alphabet_for(int qam_order, Alphabet* al) {
+    return qam_order > 0 ? make_qam_alphabet(qam_order, al) : make_lattice_alphabet(-qam_order, al);
+}
+
+// CacParams.validate (solver.py:109-124)
+static int validate(const il_cac_params* p) {
+    IL_REQUIRE(p != nullptr, "params must not be NULL");
+    IL_REQUIRE(p->dt > 0, "dt must be positive");
+    IL_REQUIRE(p->f_mvm >= 1 && p->n_steps >= 1 && p->n_anneals >= 1,
+               "f_mvm, n_steps and n_anneals must be >= 1");
+    IL_REQUIRE(p->e_floor > 0, "e_floor must be positive");
+    IL_REQUIRE(p->init_amplitude > 0, "init_amplitude must be positive");
+    const double floor_ = sqrt(fmax(fmax(p->a, p->p - 1.0), 0.0));
+    IL_REQUIRE(p->diverge_threshold > floor_,
+               "diverge_threshold must exceed sqrt(max(a, p - 1)) = %.3g", floor_);
+    IL_REQUIRE(p->precision >= IL_PREC_FP64_EXACT && p->precision <= IL_PREC_TF32,
+               "unknown precision %d", p->precision);
+    return IL_OK;
+}
+
+static AnnealScalars scalars_of(const il_cac_params* p) {
+    AnnealScalars s;
+    s.p = p->p;
+    s.a = p->a;
+    s.zeta = p->zeta;
+    s.eps = 0.0;
+    s.dt = p->dt;
+    s.e_floor = p->e_floor;
+    s.thr = p->diverge_threshold;
+    s.x0_lo = -p->init_amplitude;
+    s.x0_range = p->init_amplitude - (-p->init_amplitude);  // numpy: high - low
+    s.f_mvm = p->f_mvm;
+    s.n_steps = p->n_steps;
+    return s;
+}
+
+// One _improve_guess stage for P problems (detector.py:27-54) whose Ising
+// problems (G, g, b, offset, eps) are already built around the guess held
+// in x_idx/energy: anneal, select, decode, keep-if-strictly-better.
+static int anneal_and_select(const double* H, const double* y, int64_t P, int n_r, int n_t,
+                             const Alphabet& al, const double* G, const double* g, const double* b,
+                             const double* offset, const double* eps, const uint64_t* base,
+                             const il_cac_params* prm, uint8_t* x_idx, double* energy,
+                             int8_t* source, int32_t* anneal_index, int32_t* diverged_count,
+                             Workspace& ws, cudaStream_t st) {
+    const int N = 2 * n_t, S = 2 * N + 1, B = prm->n_anneals;
+    int rc = IL_OK;
+    int8_t* spins = ws.get<int8_t>((size_t)P * B * S, &rc);
+    uint8_t* div = ws.get<uint8_t>((size_t)P * B, &rc);
+    if (rc) return rc;
+    const AnnealScalars s = scalars_of(prm);
+    if (prm->precision != IL_PREC_FP64_EXACT && fast_anneal_supported(N, B, s)) {
+        rc = launch_anneal_fast(G, g, b, base, eps, P, N, B, s, prm->precision, spins, div, st);
+    } else {
+        rc = launch_anneal_exact(G, g, b, nullptr, base, eps, P, N, B, s, spins, div, nullptr,
+                                 nullptr, st);
+    }
+    if (rc) return rc;
+    return launch_select_decode(H, y, G, b, offset, spins, div, P, n_r, n_t, B, al, x_idx, energy,
+                                source, anneal_index, diverged_count, st);
+}
+
+}  // namespace il
+
+using namespace il;
+
+extern "C" {
+
+const char* il_last_error(void) { return il::g_err; }
+int il_abi_version(void) { return IL_ABI_VERSION; }
+
+int il_run_anneals(const double* G, const double* g_diag, const double* b, const double* x0,
+                   int32_t n_dim, int32_t n_batch, double dt, double p, double a, double zeta,
+                   double eps, double e_floor, int32_t f_mvm, int32_t n_steps,
+                   double diverge_threshold, int8_t* spins, uint8_t* diverged, int64_t* steps,
+                   int64_t* mvms, void* stream) {
+    IL_REQUIRE(n_dim >= 0 && n_batch >= 0, "negative shape");
+    IL_REQUIRE(f_mvm >= 1, "f_mvm must be >= 1");
+    IL_REQUIRE(n_batch == 0 || (x0 && spins && diverged && steps && mvms), "NULL buffer");
+    AnnealScalars s{};
+    s.p = p;
+    s.a = a;
+    s.zeta = zeta;
+    s.eps = eps;
+    s.dt = dt;
+    s.e_floor = e_floor;
+    s.thr = diverge_threshold;
+    s.f_mvm = f_mvm;
+    s.n_steps = n_steps < 0 ? 0 : n_steps;
+    return launch_anneal_exact(G, g_diag, b, x0, nullptr, nullptr, 1, n_dim, n_batch, s, spins,
+                               diverged, steps, mvms, (cudaStream_t)stream);
+}
+
+int il_run_anneals_host(const double* G, const double* g_diag, const double* b, const double* x0,
+                        int32_t n_dim, int32_t n_batch, double dt, double p, double a, double zeta,
+                        double eps, double e_floor, int32_t f_mvm, int32_t n_steps,
+                        double diverge_threshold, int8_t* spins, uint8_t* diverged,
+                        int64_t* steps, int64_t* mvms) {
+    IL_REQUIRE(n_dim >= 0 && n_batch >= 0, "negative shape");
+    const size_t N = (size_t)n_dim, S = 2 * N + 1, B = (size_t)n_batch;
+    cudaStream_t st;
+    IL_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    int rc = IL_OK;
+    {
+        Workspace ws(st);
+        double* dG = ws.get<double>(N * N, &rc);
+        double* dg = ws.get<double>(N, &rc);
+        double* db = ws.get<double>(N, &rc);
+        double* dx = ws.get<double>(B * S, &rc);
+        int8_t* ds = ws.get<int8_t>(B * S, &rc);
+        uint8_t* dd = ws.get<uint8_t>(B, &rc);
+        int64_t* dst = ws.get<int64_t>(B, &rc);
+        int64_t* dm = ws.get<int64_t>(B, &rc);
+        if (rc == IL_OK) {
+            cudaMemcpyAsync(dG, G, N * N * 8, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(dg, g_diag, N * 8, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(db, b, N * 8, cudaMemcpyHostToDevice, st);
+            cudaMemcpyAsync(dx, x0, B * S * 8, cudaMemcpyHostToDevice, st);
+            rc = il_run_anneals(dG, dg, db, dx, n_dim, n_batch, dt, p, a, zeta, eps, e_floor, f_mvm,
+                                n_steps, diverge_threshold, ds, dd, dst, dm, st);
+            if (rc == IL_OK) {
+                cudaMemcpyAsync(spins, ds, B * S, cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(diverged, dd, B, cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(steps, dst, B * 8, cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(mvms, dm, B * 8, cudaMemcpyDeviceToHost, st);
+            }
+        }
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+    if (rc == IL_OK && e != cudaSuccess) rc = fail_cuda(e, "il_run_anneals_host");
+    return rc;
+}
+
+int il_derive_seeds(const uint64_t* parts, int32_t n_parts, int64_t n, uint64_t* out,
+                    void* stream);
+int il_initial_states(const uint64_t* seeds, int64_t n, int32_t S, double amplitude, double* x0,
+                      void* stream);
+
+int il_mmse_batch(const double* H, const double* y, const double* noise_var, int64_t P,
+                  int32_t n_r, int32_t n_t, int32_t qam_order, uint8_t* x_idx, double* energy,
+                  int8_t* status, void* stream) {
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
+               "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
+    Alphabet al;
+    int rc = make_qam_alphabet(qam_order, &al);
+    if (rc) return rc;
+    return launch_mmse(H, y, noise_var, P, n_r, n_t, al, x_idx, energy, status,
+                       (cudaStream_t)stream);
+}
+
+int il_build_ising_batch(const double* H, const double* y, const uint8_t* guess_idx, int64_t P,
+                         int32_t n_r, int32_t n_t, int32_t qam_order, double* G, double* g_diag,
+                         double* b, double* offset, double* eps_scale, void* stream) {
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= 1 && n_t <= 32, "invalid shape");
+    Alphabet al;
+    int rc = alphabet_for(qam_order, &al);
+    if (rc) return rc;
+    return launch_build_ising(H, y, guess_idx, P, n_r, n_t, al, G, g_diag, b, offset, eps_scale,
+                              nullptr, 1.0, 0.0, (cudaStream_t)stream);
+}
+
+int il_detect_cim_batch(const double* H, const double* y, const double* noise_var, int64_t P,
+                        int32_t n_r, int32_t n_t, int32_t qam_order, const uint64_t* seed,
+                        const il_cac_params* prm, uint8_t* x_idx, double* energy, int8_t* source,
+                        int32_t* anneal_index, int32_t* diverged_count, void* stream) {
+    int rc = validate(prm);
+    if (rc) return rc;
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
+               "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
+    IL_REQUIRE(x_idx != nullptr, "x_idx must not be NULL");
+    Alphabet al;
+    rc = make_qam_alphabet(qam_order, &al);
+    if (rc) return rc;
+    if (P == 0) return IL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = 2 * n_t;
+    Workspace ws(st);
+    double* G = ws.get<double>((size_t)P * N * N, &rc);
+    double* g = ws.get<double>((size_t)P * N, &rc);
+    double* b = ws.get<double>((size_t)P * N, &rc);
+    double* off = ws.get<double>((size_t)P, &rc);
+    double* eps = ws.get<double>((size_t)P, &rc);
+    uint64_t* base = ws.get<uint64_t>((size_t)P, &rc);
+    double* en = energy ? energy : ws.get<double>((size_t)P, &rc);
+    int8_t* src = source ? source : ws.get<int8_t>((size_t)P, &rc);
+    if (rc) return rc;
+    const double fixed = prm->eps > 0.0 ? prm->eps : 0.0;
+    rc = launch_mmse_ising(H, y, noise_var, P, n_r, n_t, al, x_idx, en, src, G, g, b, off, eps, 1.0,
+                           fixed, st);
+    if (rc) return rc;
+    rc = launch_base_seeds(seed, P, 0, 0, base, st);  // detector.py:67 derive_seed(seed, 0, 0)
+    if (rc) return rc;
+    return anneal_and_select(H, y, P, n_r, n_t, al, G, g, b, off, eps, base, prm, x_idx, en, src,
+                             anneal_index, diverged_count, ws, st);
+}
+
+int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_u, int32_t n_ant,
+                         double power, double tau, int32_t n_stages, const uint64_t* seed,
+                         const il_cac_params* prm, double* x, double* v, double* unnorm_power,
+                         int32_t* diverged_count, void* stream) {
+    int rc = validate(prm);
+    if (rc) return rc;
+    IL_REQUIRE(power > 0, "P must be positive");
+    IL_REQUIRE(n_u >= 1 && n_u <= n_ant && n_u <= 32 && n_ant <= 64,
+               "downlink precoding requires 1 <= n_u <= n_ant (n_u <= 32, n_ant <= 64)");
+    Alphabet al;
+    rc = make_lattice_alphabet(n_stages, &al);
+    if (rc) return rc;
+    if (P == 0) return IL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = 2 * n_u;
+    Workspace ws(st);
+    double* W = ws.get<double>((size_t)P * n_ant * n_u * 2, &rc);
+    double* Hp = ws.get<double>((size_t)P * n_ant * n_u * 2, &rc);
+    double* yt = ws.get<double>((size_t)P * n_ant * 2, &rc);
+    double* base_e = ws.get<double>((size_t)P, &rc);
+    double* en = ws.get<double>((size_t)P, &rc);
+    int8_t* status = ws.get<int8_t>((size_t)P, &rc);
+    uint8_t* vidx = ws.get<uint8_t>((size_t)P * 2 * n_u, &rc);
+    double* G = ws.get<double>((size_t)P * N * N, &rc);
+    double* g = ws.get<double>((size_t)P * N, &rc);
+    double* b = ws.get<double>((size_t)P * N, &rc);
+    double* off = ws.get<double>((size_t)P, &rc);
+    double* eps = ws.get<double>((size_t)P, &rc);
+    uint64_t* base = ws.get<uint64_t>((size_t)P, &rc);
+    int32_t* stage_div = diverged_count ? ws.get<int32_t>((size_t)P, &rc) : nullptr;
+    if (rc) return rc;
+    rc = launch_zf_vpp_front(H, u, P, n_u, n_ant, tau, W, yt, Hp, base_e, status, st);
+    if (rc) return rc;
+    IL_CHECK_CUDA(cudaMemsetAsync(vidx, n_stages, (size_t)P * 2 * n_u, st));  // vhat = 0
+    IL_CHECK_CUDA(cudaMemcpyAsync(en, base_e, (size_t)P * 8, cudaMemcpyDeviceToDevice, st));
+    if (diverged_count) IL_CHECK_CUDA(cudaMemsetAsync(diverged_count, 0, (size_t)P * 4, st));
+    const double fixed = prm->eps > 0.0 ? prm->eps : 0.0;
+    for (int stage = 0; stage < n_stages; ++stage) {
+        // precoder.py:115-124: _improve_guess(..., derive_seed(seed, 0, stage), eps_gain=1/16)
+        rc = launch_build_ising(Hp, yt, vidx, P, n_ant, n_u, al, G, g, b, off, nullptr, eps,
+                                0.0625, fixed, st);
+        if (rc) return rc;
+        rc = launch_base_seeds(seed, P, 0, (uint64_t)stage, base, st);
+        if (rc) return rc;
+        rc = anneal_and_select(Hp, yt, P, n_ant, n_u, al, G, g, b, off, eps, base, prm, vidx, en,
+                               nullptr, nullptr, stage_div, ws, st);
+        if (rc) return rc;
+        if (diverged_count) {
+            rc = launch_add_i32(stage_div, P, diverged_count, st);
+            if (rc) return rc;
+        }
+    }
+    return launch_vpp_post(W, u, yt, base_e, vidx, P, n_u, n_ant, n_stages, tau, power, x, v,
+                           unnorm_power, st);
+}
+
+int il_gray_demap(const uint8_t* x_idx, int64_t n_sym, int32_t bits_per_dim, uint8_t* bits,
+                  void* stream) {
+    return launch_gray_demap(x_idx, n_sym, bits_per_dim, bits, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,382 @@
+// Throughput CIM-CAC anneal kernel: FP32 state in registers, coupling
+// product on the tensor cores, state never leaves the register file.
+//
+// Dynamics (reference _kernel.pyx:64-97):
+//   every f_mvm steps:  m = G (x1 + x2);  c1 = m - g.x1 + b xa;  c2 = m - g.x2 + b xa;
+//                       c_aux = b.(x1 + x2)
+//   every step:         x += dt((p-1)x - x^3 - eps e c);   e = max(e_floor, e - dt zeta (x^2 - a) e)
+//
+// Mapping (one warp = 16 anneals of one problem, N = 8*NT spins per half):
+//   The refresh is the small GEMM  M^T[a][i] = sum_j V^T[a][j] G[j][i]  with
+//   a = anneal (MMA M dimension), i = spin (N dimension), j = spin (K).  It is
+//   issued as mma.sync.m16n8k8 TF32 tiles.  Thread (g = lane/4, t = lane%4)
+//   owns anneals {g, g+8} and, in every n-tile n, spins {8n+2t, 8n+2t+1} of
+//   both halves: exactly the accumulator (C) fragment of the tile.  The A
+//   fragment of k-tile k wants columns {t, t+4}; ordering the K dimension of
+//   tile k as (8k+0, 8k+2, 8k+4, 8k+6, 8k+1, 8k+3, 8k+5, 8k+7) makes those
+//   columns spins {8k+2t, 8k+2t+1} -- the thread's own.  G's B fragments are
+//   staged once per problem in that permuted order, so a refresh moves no
+//   data between lanes at all: v = x1 + x2 is formed in registers, fed to
+//   the MMA, and the result lands where the Euler update needs it.
+//   IL_PREC_FP32 splits both operands into TF32 hi + lo parts (3 MMAs per
+//   tile: hi*hi + lo*hi + hi*lo), giving FP32-level accuracy; IL_PREC_TF32
+//   uses one pass.
+//   The Euler update runs on packed FP32x2 (FFMA2/FMUL2) over spin pairs.
+//   The aux spin (one per anneal) is integrated redundantly and bit-identically
+//   by the 4 lanes of a quad; c_aux comes from a quad shuffle reduction.
+//
+// Divergence: a per-anneal sticky max of x^2 (NaN-propagating), which yields
+// exactly the reference's `diverged` flag; spins of a diverged anneal are not
+// frozen at the halting step, which is harmless because diverged anneals are
+// excluded from selection (solver.py:262-264).  The exact kernel serves the
+// drop-in run_anneals path where frozen spins are part of the contract.
+//
+// Scaling: G, g, b are pre-multiplied by -dt*eps so that the MMA directly
+// yields the -dt*eps*c term of the update.
+#include <mma.h>
+
+#include "il_internal.cuh"
+#include "rng_numpy.cuh"
+
+namespace il {
+
+namespace {
+
+constexpr int kWarpsPerCta = 4;
+
+struct FastScalars {
+    float alpha;    // 1 + dt (p - 1)
+    float ndt;      // -dt
+    float beta;     // 1 + dt zeta a
+    float ndtz;     // -dt zeta
+    float e_floor;
+    float thr2;     // diverge_threshold^2
+    double dt;
+    double x0_lo, x0_range;
+    U128 jump_mult, jump_add;  // PCG64 advance by half the stream
+    int f_mvm, n_steps;
+};
+
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float max_nan3(float a, float b, float c) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    asm("max.NaN.f32 %0, %0, %1;" : "+f"(r) : "f"(c));
+    return r;
+}
+__device__ __forceinline__ float max_nan(float a, float b) {
+    float r;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+// One explicit-Euler step of a spin pair (packed FP32x2).
+//   x' = x (alpha - dt x^2) + e C      (C = -dt eps c)
+//   e' = max(e_floor, e (beta - dt zeta x^2))
+// x2 of the incoming state is folded into the divergence max.
+__device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
+                                           const FastScalars& s, float& dv) {
+    const float2 x2 = __fmul2_rn(x, x);
+    dv = max_nan3(dv, x2.x, x2.y);
+    const float2 q = __ffma2_rn(make_float2(s.ndt, s.ndt), x2, make_float2(s.alpha, s.alpha));
+    const float2 r = __ffma2_rn(make_float2(s.ndtz, s.ndtz), x2, make_float2(s.beta, s.beta));
+    const float2 t = __fmul2_rn(x, q);
+    x = __ffma2_rn(e, C, t);
+    const float2 er = __fmul2_rn(e, r);
+    e = make_float2(fmaxf(er.x, s.e_floor), fmaxf(er.y, s.e_floor));
+}
+
+__device__ __forceinline__ void euler_one(float& x, float& e, const float C, const FastScalars& s,
+                                          float& dv) {
+    const float x2 = x * x;
+    dv = max_nan(dv, x2);
+    const float q = fmaf(s.ndt, x2, s.alpha);
+    const float r = fmaf(s.ndtz, x2, s.beta);
+    x = fmaf(e, C, x * q);
+    e = fmaxf(e * r, s.e_floor);
+}
+
+template <int NT, bool SPLIT>
+__global__ void __launch_bounds__(kWarpsPerCta * 32)
+k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
+              const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
+              const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
+              FastScalars s, int8_t* __restrict__ spins, uint8_t* __restrict__ diverged) {
+    constexpr int N = 8 * NT;
+    constexpr int S = 2 * N + 1;
+    // per warp: G fragments [NT][NT][32] x float4 (hi0, hi1, lo0, lo1) + x0 staging [16][S]
+    extern __shared__ __align__(16) float4 smem_f4[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t task = (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    if (task >= n_tasks) return;
+    const int64_t prob = task / tiles_per_prob;
+    const int mt = (int)(task % tiles_per_prob);
+    const int B = tiles_per_prob * 16;
+    float4* frag = smem_f4 + warp * (NT * NT * 32 + (16 * S + 3) / 4);
+    float* x0s = reinterpret_cast<float*>(frag + NT * NT * 32);
+
+    const int g = lane >> 2, t = lane & 3;
+    const double K = s.dt * eps_p[prob];
+    const double* G = Gall + prob * (int64_t)N * N;
+
+    // ---- stage -K*G as permuted TF32 B fragments (hi, lo) ------------------
+#pragma unroll
+    for (int kt = 0; kt < NT; ++kt) {
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const float f0 = (float)(-K * __ldg(G + (8 * kt + 2 * t) * N + 8 * n + g));
+            const float f1 = (float)(-K * __ldg(G + (8 * kt + 2 * t + 1) * N + 8 * n + g));
+            const uint32_t h0 = to_tf32(f0), h1 = to_tf32(f1);
+            const uint32_t l0 = to_tf32(f0 - __uint_as_float(h0));
+            const uint32_t l1 = to_tf32(f1 - __uint_as_float(h1));
+            frag[(kt * NT + n) * 32 + lane] = make_float4(__uint_as_float(h0), __uint_as_float(h1),
+                                                          __uint_as_float(l0), __uint_as_float(l1));
+        }
+    }
+    // per-thread spin constants: K g_i and -K b_i for spins 8n+2t+{0,1}
+    float2 Kg[NT], nKb[NT];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        const int i = 8 * n + 2 * t;
+        Kg[n] = make_float2((float)(K * gall[prob * N + i]), (float)(K * gall[prob * N + i + 1]));
+        nKb[n] = make_float2((float)(-K * ball[prob * N + i]), (float)(-K * ball[prob * N + i + 1]));
+    }
+
+    // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
+    {
+        const int al = lane & 15, part = lane >> 4;
+        const int a = mt * 16 + al;
+        Pcg64 rng;
+        rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)a));
+        constexpr int S0 = (S + 1) / 2;
+        if (part) rng.state = add128(mul128(rng.state, s.jump_mult), mul128(rng.inc, s.jump_add));
+        const int i0 = part ? S0 : 0, i1 = part ? S : S0;
+        for (int i = i0; i < i1; ++i) x0s[al * S + i] = (float)rng.uniform(s.x0_lo, s.x0_range);
+    }
+    __syncwarp();
+
+    float2 xA[2][NT], xB[2][NT], eA[2][NT], eB[2][NT], CA[2][NT], CB[2][NT];
+    float xa[2], ea[2], Ca[2], dv[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float* r = x0s + (g + 8 * h) * S;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const int i = 8 * n + 2 * t;
+            xA[h][n] = make_float2(r[i], r[i + 1]);
+            xB[h][n] = make_float2(r[N + i], r[N + i + 1]);
+            eA[h][n] = eB[h][n] = make_float2(1.f, 1.f);
+            CA[h][n] = CB[h][n] = make_float2(0.f, 0.f);
+        }
+        xa[h] = r[2 * N];
+        ea[h] = 1.f;
+        Ca[h] = 0.f;
+        dv[h] = 0.f;
+    }
+
+    for (int step = 0; step < s.n_steps; ++step) {
+        if (step % s.f_mvm == 0) {
+            // ---- refresh: v = x1 + x2, M' = -K G v on tensor cores ------------
+            float2 v[2][NT];
+            float pb[2] = {0.f, 0.f};
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    v[h][n] = __fadd2_rn(xA[h][n], xB[h][n]);
+                    pb[h] = fmaf(nKb[n].x, v[h][n].x, pb[h]);
+                    pb[h] = fmaf(nKb[n].y, v[h][n].y, pb[h]);
+                }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                pb[h] += __shfl_xor_sync(0xffffffffu, pb[h], 1);
+                pb[h] += __shfl_xor_sync(0xffffffffu, pb[h], 2);
+                Ca[h] = pb[h];
+            }
+            float acc[NT][4];
+#pragma unroll
+            for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+#pragma unroll
+            for (int kt = 0; kt < NT; ++kt) {
+                const float av[4] = {v[0][kt].x, v[1][kt].x, v[0][kt].y, v[1][kt].y};
+                uint32_t ahi[4], alo[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    ahi[q] = to_tf32(av[q]);
+                    alo[q] = to_tf32(av[q] - __uint_as_float(ahi[q]));
+                }
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const float4 f = frag[(kt * NT + n) * 32 + lane];
+                    if (SPLIT) {
+                        mma_tf32(acc[n], alo, __float_as_uint(f.x), __float_as_uint(f.y));
+                        mma_tf32(acc[n], ahi, __float_as_uint(f.z), __float_as_uint(f.w));
+                    }
+                    mma_tf32(acc[n], ahi, __float_as_uint(f.x), __float_as_uint(f.y));
+                }
+            }
+            // ---- coupling assembly: C = M' + K g x_self - K b xa -------------
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const float2 m2 = make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
+                    const float2 u2 = __ffma2_rn(nKb[n], make_float2(xa[h], xa[h]), m2);
+                    CA[h][n] = __ffma2_rn(Kg[n], xA[h][n], u2);
+                    CB[h][n] = __ffma2_rn(Kg[n], xB[h][n], u2);
+                }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                euler_pair(xA[h][n], eA[h][n], CA[h][n], s, dv[h]);
+                euler_pair(xB[h][n], eB[h][n], CB[h][n], s, dv[h]);
+            }
+            euler_one(xa[h], ea[h], Ca[h], s, dv[h]);
+        }
+    }
+
+    // ---- final divergence check, spins out ---------------------------------
+    const int64_t row0 = prob * (int64_t)B + mt * 16;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        float d = dv[h];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            d = max_nan3(d, xA[h][n].x * xA[h][n].x, xA[h][n].y * xA[h][n].y);
+            d = max_nan3(d, xB[h][n].x * xB[h][n].x, xB[h][n].y * xB[h][n].y);
+        }
+        d = max_nan(d, xa[h] * xa[h]);
+        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 1));
+        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 2));
+        const int64_t row = row0 + g + 8 * h;
+        int8_t* sp = spins + row * S;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const int i = 8 * n + 2 * t;
+            char2 sa, sb;
+            sa.x = xA[h][n].x >= 0.f ? 1 : -1;
+            sa.y = xA[h][n].y >= 0.f ? 1 : -1;
+            sb.x = xB[h][n].x >= 0.f ? 1 : -1;
+            sb.y = xB[h][n].y >= 0.f ? 1 : -1;
+            sp[i] = sa.x;
+            sp[i + 1] = sa.y;
+            sp[N + i] = sb.x;
+            sp[N + i + 1] = sb.y;
+        }
+        if (t == 0) {
+            sp[2 * N] = xa[h] >= 0.f ? 1 : -1;
+            diverged[row] = (d <= s.thr2) ? 0 : 1;
+        }
+    }
+}
+
+template <int NT>
+size_t fast_smem(int) {
+    constexpr int S = 16 * NT + 1;
+    return sizeof(float4) * kWarpsPerCta * (NT * NT * 32 + (16 * S + 3) / 4);
+}
+
+template <int NT>
+int launch_nt(const double* G, const double* g, const double* b, const uint64_t* base_seed,
+              const double* eps_p, int64_t P, int B, const FastScalars& fs, bool split,
+              int8_t* spins, uint8_t* diverged, cudaStream_t st) {
+    const int tiles = B / 16;
+    const int64_t n_tasks = P * tiles;
+    const int64_t blocks = (n_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
+    IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
+    const size_t smem = fast_smem<NT>(0);
+    if (split) {
+        IL_CHECK_CUDA(cudaFuncSetAttribute(k_anneal_fast<NT, true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_anneal_fast<NT, true><<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(
+            G, g, b, base_seed, eps_p, n_tasks, tiles, fs, spins, diverged);
+    } else {
+        IL_CHECK_CUDA(cudaFuncSetAttribute(k_anneal_fast<NT, false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_anneal_fast<NT, false><<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(
+            G, g, b, base_seed, eps_p, n_tasks, tiles, fs, spins, diverged);
+    }
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+// PCG64 advance-by-k constants: state_k = M^k state_0 + inc * (M^{k-1} + ... + 1)
+void pcg_jump(int k, U128* mult, U128* add) {
+    const U128 M = {0x2360ED051FC65DA4ull, 0x4385DF649FCCF645ull};
+    U128 pm = {0, 1}, sum = {0, 0};
+    for (int i = 0; i < k; ++i) {
+        sum = add128(sum, pm);
+        pm = mul128(pm, M);
+    }
+    *mult = pm;
+    *add = sum;
+}
+
+}  // namespace
+
+bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
+    if (N % 8 != 0 || N < 8 || N > 64 || B % 16 != 0 || B <= 0) return false;
+    // the aux/initial-state check folds x0 into the sticky max: require |x0| < thr
+    if (!(s.x0_range * 0.5 < s.thr)) return false;
+    // e may not overflow FP32 while x stays below the threshold
+    const double thr2 = s.thr * s.thr;
+    const double r1 = fabs(1.0 + s.dt * s.zeta * s.a);
+    const double r2 = fabs(1.0 - s.dt * s.zeta * (thr2 - s.a));
+    const double rmax = fmax(r1, r2);
+    if (rmax > 1.0 && (double)s.n_steps * log(rmax) > 80.0) return false;
+    return true;
+}
+
+int launch_anneal_fast(const double* G, const double* g, const double* b,
+                       const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
+                       const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
+                       cudaStream_t st) {
+    if (!fast_anneal_supported(N, B, s)) {
+        set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
+        return IL_ERR_UNSUPPORTED;
+    }
+    if (P == 0) return IL_OK;
+    FastScalars fs;
+    fs.alpha = (float)(1.0 + s.dt * (s.p - 1.0));
+    fs.ndt = (float)(-s.dt);
+    fs.beta = (float)(1.0 + s.dt * s.zeta * s.a);
+    fs.ndtz = (float)(-s.dt * s.zeta);
+    fs.e_floor = (float)s.e_floor;
+    fs.thr2 = (float)(s.thr * s.thr);
+    fs.dt = s.dt;
+    fs.x0_lo = s.x0_lo;
+    fs.x0_range = s.x0_range;
+    fs.f_mvm = s.f_mvm;
+    fs.n_steps = s.n_steps;
+    pcg_jump((2 * N + 2) / 2, &fs.jump_mult, &fs.jump_add);
+    const bool split = precision != IL_PREC_TF32;
+    switch (N / 8) {
+        case 1: return launch_nt<1>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        case 2: return launch_nt<2>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        case 3: return launch_nt<3>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        case 4: return launch_nt<4>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        case 6: return launch_nt<6>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        case 8: return launch_nt<8>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        default:
+            set_error("fast anneal kernel not instantiated for n_dim=%d", N);
+            return IL_ERR_UNSUPPORTED;
+    }
+}
+
+}  // namespace il

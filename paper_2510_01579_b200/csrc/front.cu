@@ -1,0 +1,778 @@
+// FP64 per-problem reduction kernels: MMSE front-end, Ising reduction with
+// lambda_max, ZF/VPP front-end, and the selection/decode epilogue.
+//
+// One warp owns one problem (a resource element); its matrices live in a
+// warp-private slice of shared memory, lanes own rows.  Everything here is
+// FP64 because the hard decisions must match the reference: an FP32 MMSE
+// flips 1-3 decisions per 10^4 REs at 16x16.
+//
+// Reference map:
+//   mmse front      linear.py:55-75        (A = H^H H + s2 I, Cholesky solve, project)
+//   build_ising     transform.py:97-140    (G, g_diag, b, offset, eps_scale)
+//   lambda_max      transform.py:126       (eigvalsh(G)[-1] = c^2 lambda_max(H^H H))
+//   zf / vpp front  precoder.py:54-60, 93-125
+//   select/decode   solver.py:256-279, detector.py:44-54, transform.py:155-169
+//   vpp post        precoder.py:126-146
+#include <float.h>
+
+#include "il_internal.cuh"
+#include "rng_numpy.cuh"
+
+namespace il {
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ---------------------------------------------------------------------------
+// warp-cooperative FP64 linear algebra on shared-memory matrices (row-major)
+// ---------------------------------------------------------------------------
+
+// A[n_t x n_t] = H^H H (exactly Hermitian: upper half computed, mirrored),
+// z[n_t] = H^H y.  H is [n_r x n_t].
+__device__ void gram_hermitian(const cplx* H, const cplx* y, int n_r, int n_t, cplx* A, cplx* z,
+                               int lane) {
+    for (int idx = lane; idx < n_t * n_t; idx += 32) {
+        const int i = idx / n_t, j = idx % n_t;
+        if (i > j) continue;
+        double re = 0.0, im = 0.0;
+        for (int k = 0; k < n_r; ++k) {
+            const cplx hi = H[k * n_t + i], hj = H[k * n_t + j];
+            re += hi.re * hj.re + hi.im * hj.im;
+            im += hi.re * hj.im - hi.im * hj.re;
+        }
+        if (i == j) im = 0.0;
+        A[i * n_t + j] = {re, im};
+        A[j * n_t + i] = {re, -im};
+    }
+    if (y) {
+        for (int i = lane; i < n_t; i += 32) {
+            double re = 0.0, im = 0.0;
+            for (int k = 0; k < n_r; ++k) {
+                const cplx h = H[k * n_t + i], v = y[k];
+                re += h.re * v.re + h.im * v.im;
+                im += h.re * v.im - h.im * v.re;
+            }
+            z[i] = {re, im};
+        }
+    }
+    __syncwarp();
+}
+
+// In-place lower Cholesky M = L L^H (M Hermitian positive definite, n <= 32,
+// lane i owns row i).  Returns false on a non-positive pivot (the reference
+// raises LinAlgError from cho_factor in that case).
+__device__ bool cholesky_lower(cplx* M, int n, int lane) {
+    for (int k = 0; k < n; ++k) {
+        const double piv = M[k * n + k].re;
+        if (!(piv > 0.0)) return false;
+        const double lkk = sqrt(piv);
+        __syncwarp();
+        if (lane > k && lane < n) {
+            cplx v = M[lane * n + k];
+            M[lane * n + k] = {v.re / lkk, v.im / lkk};
+        }
+        __syncwarp();
+        if (lane == k) M[k * n + k] = {lkk, 0.0};
+        if (lane > k && lane < n) {
+            const cplx lik = M[lane * n + k];
+            for (int j = k + 1; j <= lane; ++j) {
+                const cplx ljk = M[j * n + k];
+                // M[i][j] -= L[i][k] * conj(L[j][k])
+                M[lane * n + j].re -= lik.re * ljk.re + lik.im * ljk.im;
+                M[lane * n + j].im -= lik.im * ljk.re - lik.re * ljk.im;
+            }
+        }
+        __syncwarp();
+    }
+    return true;
+}
+
+// Solve (L L^H) x = rhs in place (rhs -> x); L lower from cholesky_lower.
+__device__ void cholesky_solve(const cplx* L, int n, cplx* x, int lane) {
+    for (int k = 0; k < n; ++k) {  // L w = rhs
+        __syncwarp();
+        const double lkk = L[k * n + k].re;
+        const cplx wk = {x[k].re / lkk, x[k].im / lkk};
+        __syncwarp();
+        if (lane == k) x[k] = wk;
+        if (lane > k && lane < n) x[lane] = csub(x[lane], cmul(L[lane * n + k], wk));
+    }
+    for (int k = n - 1; k >= 0; --k) {  // L^H x = w
+        __syncwarp();
+        const double lkk = L[k * n + k].re;
+        const cplx xk = {x[k].re / lkk, x[k].im / lkk};
+        __syncwarp();
+        if (lane == k) x[k] = xk;
+        if (lane < k) x[lane] = csub(x[lane], cmulc(L[k * n + lane], xk));
+    }
+    __syncwarp();
+}
+
+// Largest eigenvalue of the Hermitian A[n x n] (destroyed): Householder
+// reduction to real symmetric tridiagonal form, then warp-parallel
+// multisection on the Sturm count (32 probes per round, ~11 rounds to full
+// FP64 resolution).  scratch: 3*n cplx + 2*n double.
+__device__ double lambda_max_hermitian(cplx* A, int n, cplx* scratch, int lane) {
+    cplx* v = scratch;
+    cplx* p = v + n;
+    cplx* w = p + n;
+    double* d = reinterpret_cast<double*>(w + n);
+    double* e = d + n;
+    for (int k = 0; k + 2 < n; ++k) {
+        const int m = n - k - 1;
+        cplx xi = {0.0, 0.0};
+        if (lane < m) xi = A[(k + 1 + lane) * n + k];
+        const double sig2 = warp_sum(cabs2(xi));
+        if (lane == 0) d[k] = A[k * n + k].re;
+        if (!(sig2 > 0.0)) {
+            if (lane == 0) e[k] = 0.0;
+            __syncwarp();
+            continue;
+        }
+        const double sig = sqrt(sig2);
+        const cplx x0 = A[(k + 1) * n + k];
+        const double ax0 = sqrt(cabs2(x0));
+        const cplx ph = ax0 > 0.0 ? cplx{x0.re / ax0, x0.im / ax0} : cplx{1.0, 0.0};
+        const double tau = 1.0 / (sig * (sig + ax0));
+        if (lane < m) v[lane] = lane == 0 ? cplx{xi.re + ph.re * sig, xi.im + ph.im * sig} : xi;
+        if (lane == 0) e[k] = sig;
+        __syncwarp();
+        cplx pi = {0.0, 0.0};
+        if (lane < m) {
+            const cplx* Bi = A + (k + 1 + lane) * n + (k + 1);
+            for (int j = 0; j < m; ++j) pi = cadd(pi, cmul(Bi[j], v[j]));
+            pi = {tau * pi.re, tau * pi.im};
+        }
+        // K = (tau/2) v^H p  (real for Hermitian B)
+        const double vhp = warp_sum(lane < m ? v[lane].re * pi.re + v[lane].im * pi.im : 0.0);
+        const double K = 0.5 * tau * vhp;
+        if (lane < m) w[lane] = {pi.re - K * v[lane].re, pi.im - K * v[lane].im};
+        __syncwarp();
+        if (lane < m) {
+            const cplx vi = v[lane], wi = w[lane];
+            cplx* Bi = A + (k + 1 + lane) * n + (k + 1);
+            for (int j = 0; j < m; ++j) {
+                // B[i][j] -= v_i conj(w_j) + w_i conj(v_j)
+                const cplx a1 = cmulc(w[j], vi);  // conj(w_j) * v_i
+                const cplx a2 = cmulc(v[j], wi);
+                Bi[j] = csub(Bi[j], cadd(a1, a2));
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (n >= 2) {
+            d[n - 2] = A[(n - 2) * n + (n - 2)].re;
+            e[n - 2] = sqrt(cabs2(A[(n - 1) * n + (n - 2)]));
+        }
+        d[n - 1] = A[(n - 1) * n + (n - 1)].re;
+    }
+    __syncwarp();
+    if (n == 1) return d[0];
+
+    // Gershgorin interval
+    double lo = DBL_MAX, hi = -DBL_MAX, emax2 = 0.0;
+    for (int i = 0; i < n; ++i) {
+        const double r = (i > 0 ? e[i - 1] : 0.0) + (i < n - 1 ? e[i] : 0.0);
+        lo = fmin(lo, d[i] - r);
+        hi = fmax(hi, d[i] + r);
+        if (i < n - 1) emax2 = fmax(emax2, e[i] * e[i]);
+    }
+    const double pivmin = DBL_MIN * fmax(1.0, emax2);
+    const double span = fmax(hi - lo, DBL_MIN);
+    lo -= 2.0 * DBL_EPSILON * span;
+    hi += 2.0 * DBL_EPSILON * span;
+    for (int round = 0; round < 24; ++round) {
+        const double step = (hi - lo) / 33.0;
+        const double xl = lo + step * (double)(lane + 1);
+        // Sturm count of eigenvalues < xl
+        int cnt = 0;
+        double q = d[0] - xl;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+        for (int i = 1; i < n; ++i) {
+            q = (d[i] - xl) - (e[i - 1] * e[i - 1]) / q;
+            if (fabs(q) < pivmin) q = -pivmin;
+            cnt += q < 0.0;
+        }
+        const unsigned above = __ballot_sync(kFull, cnt == n);
+        double nlo, nhi;
+        if (above == 0u) {
+            nlo = __shfl_sync(kFull, xl, 31);
+            nhi = hi;
+        } else {
+            const int l = __ffs(above) - 1;
+            nhi = __shfl_sync(kFull, xl, l);
+            nlo = l > 0 ? __shfl_sync(kFull, xl, l - 1) : lo;
+        }
+        const bool stalled = (nlo == lo && nhi == hi);
+        lo = nlo;
+        hi = nhi;
+        if (stalled || hi - lo <= 4.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) break;
+    }
+    return 0.5 * (lo + hi);
+}
+
+// Per-warp shared-memory carve-up for the detection front-end.
+struct FrontSmem {
+    cplx *H, *y, *A, *M, *z, *r, *scr;
+    IL_HD static size_t bytes(int n_r, int n_t) {
+        const size_t c = (size_t)n_r * n_t + n_r + 2 * (size_t)n_t * n_t + n_t + n_r + 5 * n_t + 4;
+        return c * sizeof(cplx);
+    }
+    __device__ void carve(char* base, int n_r, int n_t) {
+        H = reinterpret_cast<cplx*>(base);
+        y = H + n_r * n_t;
+        A = y + n_r;
+        M = A + n_t * n_t;
+        z = M + n_t * n_t;
+        r = z + n_t;
+        scr = r + n_r;
+    }
+};
+
+__device__ void load_problem(const double* Hg, const double* yg, int64_t prob, int n_r, int n_t,
+                             cplx* H, cplx* y, int lane) {
+    const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n_t;
+    for (int i = lane; i < n_r * n_t; i += 32) H[i] = Hp[i];
+    const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
+    for (int i = lane; i < n_r; i += 32) y[i] = yp[i];
+    __syncwarp();
+}
+
+// r = y - H x_g (x_g from level indices), returns ||r||^2 on every lane.
+__device__ double residual_from_idx(const cplx* H, const cplx* y, const uint8_t* idx, int n_r,
+                                    int n_t, const Alphabet& al, cplx* r, int lane) {
+    double acc = 0.0;
+    for (int k = lane; k < n_r; k += 32) {
+        cplx s = {0.0, 0.0};
+        for (int j = 0; j < n_t; ++j) {
+            const cplx xj = {al.levels[idx[2 * j]], al.levels[idx[2 * j + 1]]};
+            s = cadd(s, cmul(H[k * n_t + j], xj));
+        }
+        const cplx rk = csub(y[k], s);
+        r[k] = rk;
+        acc += cabs2(rk);
+    }
+    __syncwarp();
+    return warp_sum(acc);
+}
+
+struct IsingOut {
+    double *G, *g, *b, *offset, *eps_scale, *eps_out;
+    double eps_gain, fixed_eps;
+};
+
+// G, g_diag, b, offset, eps_scale around the guess whose residual is r (r2 = ||r||^2).
+__device__ void emit_ising(cplx* H, const cplx* r, double r2, cplx* A, cplx* scr, int n_r, int n_t,
+                           const Alphabet& al, int64_t prob, const IsingOut& o, int lane) {
+    const int N = 2 * n_t;
+    const double c = 0.5 * al.spacing;
+    const double c2 = c * c;
+    double* G = o.G + prob * (int64_t)N * N;
+    for (int idx = lane; idx < N * N; idx += 32) {
+        const int i = idx / N, j = idx % N;
+        const cplx aij = A[(i % n_t) * n_t + (j % n_t)];
+        double v;
+        if ((i < n_t) == (j < n_t)) v = aij.re;
+        else v = (i < n_t) ? -aij.im : aij.im;
+        G[idx] = c2 * v;
+    }
+    double tr = 0.0;
+    for (int i = lane; i < n_t; i += 32) {
+        const double gi = c2 * A[i * n_t + i].re;
+        if (o.g) {
+            o.g[prob * N + i] = gi;
+            o.g[prob * N + n_t + i] = gi;
+        }
+        tr += 2.0 * gi;
+        // H^H r
+        double re = 0.0, im = 0.0;
+        for (int k = 0; k < n_r; ++k) {
+            const cplx h = H[k * n_t + i], v = r[k];
+            re += h.re * v.re + h.im * v.im;
+            im += h.re * v.im - h.im * v.re;
+        }
+        o.b[prob * N + i] = -c * re;
+        o.b[prob * N + n_t + i] = -c * im;
+    }
+    tr = warp_sum(tr);
+    __syncwarp();
+    const double lam_a = lambda_max_hermitian(A, n_t, scr, lane);
+    if (lane == 0) {
+        if (o.offset) o.offset[prob] = r2 + 2.0 * tr;
+        const double lam = c2 * lam_a;
+        const double S = (double)(2 * N + 1);
+        const double es = 32.0 / sqrt(fmax(lam, 1e-30) * S);
+        if (o.eps_scale) o.eps_scale[prob] = es;
+        if (o.eps_out) o.eps_out[prob] = o.fixed_eps > 0.0 ? o.fixed_eps : es * o.eps_gain;
+    }
+    __syncwarp();
+}
+
+// Detection front-end.  DO_MMSE: guess = projected MMSE solution (written to
+// x_idx, energy); else guess read from x_idx.  DO_ISING: emit the Ising problem.
+template <bool DO_MMSE, bool DO_ISING>
+__global__ void k_front(const double* __restrict__ Hg, const double* __restrict__ yg,
+                        const double* __restrict__ s2g, int64_t P, int n_r, int n_t, Alphabet al,
+                        uint8_t* __restrict__ x_idx, double* __restrict__ energy,
+                        int8_t* __restrict__ status, IsingOut o) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (prob >= P) return;
+    FrontSmem sm;
+    sm.carve(smem_raw + warp * FrontSmem::bytes(n_r, n_t), n_r, n_t);
+    load_problem(Hg, yg, prob, n_r, n_t, sm.H, sm.y, lane);
+    gram_hermitian(sm.H, sm.y, n_r, n_t, sm.A, sm.z, lane);
+    uint8_t* idx = x_idx + prob * 2 * n_t;
+    if (DO_MMSE) {
+        const double s2 = s2g[prob];
+        for (int i = lane; i < n_t * n_t; i += 32) {
+            cplx a = sm.A[i];
+            if (i / n_t == i % n_t) a.re += s2;
+            sm.M[i] = a;
+        }
+        __syncwarp();
+        const bool ok = cholesky_lower(sm.M, n_t, lane);
+        if (status && lane == 0) status[prob] = ok ? 0 : -1;
+        if (ok) {
+            cholesky_solve(sm.M, n_t, sm.z, lane);
+            for (int j = lane; j < n_t; j += 32) {
+                idx[2 * j] = (uint8_t)level_index(sm.z[j].re, al);
+                idx[2 * j + 1] = (uint8_t)level_index(sm.z[j].im, al);
+            }
+        } else {
+            for (int j = lane; j < 2 * n_t; j += 32) idx[j] = 0;
+        }
+        __syncwarp();
+    }
+    const double r2 = residual_from_idx(sm.H, sm.y, idx, n_r, n_t, al, sm.r, lane);
+    if (energy && lane == 0) energy[prob] = r2;
+    if (DO_ISING) emit_ising(sm.H, sm.r, r2, sm.A, sm.scr, n_r, n_t, al, prob, o, lane);
+}
+
+int front_blocks(int64_t P, size_t per_warp, int* wpb, size_t* smem) {
+    int w = (int)((200 * 1024) / per_warp);
+    w = w < 1 ? 1 : (w > 4 ? 4 : w);
+    *wpb = w;
+    *smem = per_warp * w;
+    return (int)((P + w - 1) / w);
+}
+
+// ---------------------------------------------------------------------------
+// selection / decode epilogue
+// ---------------------------------------------------------------------------
+__global__ void k_select_decode(const double* __restrict__ Hg, const double* __restrict__ yg,
+                                const double* __restrict__ Gg, const double* __restrict__ bg,
+                                const double* __restrict__ offset, const int8_t* __restrict__ spins,
+                                const uint8_t* __restrict__ diverged, int64_t P, int n_r, int n_t,
+                                int B, Alphabet al, uint8_t* __restrict__ x_idx,
+                                double* __restrict__ energy, int8_t* __restrict__ source,
+                                int32_t* __restrict__ anneal_index,
+                                int32_t* __restrict__ diverged_count) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (prob >= P) return;
+    const int N = 2 * n_t, S = 2 * N + 1;
+    const size_t per_warp = sizeof(double) * ((size_t)N * N + N) + sizeof(cplx) * ((size_t)n_r * n_t + n_r);
+    char* base = smem_raw + warp * ((per_warp + 15) / 16 * 16);
+    double* G = reinterpret_cast<double*>(base);
+    double* b = G + N * N;
+    cplx* H = reinterpret_cast<cplx*>(b + N);
+    cplx* y = H + n_r * n_t;
+    const double* Gp = Gg + prob * (int64_t)N * N;
+    for (int i = lane; i < N * N; i += 32) G[i] = Gp[i];
+    for (int i = lane; i < N; i += 32) b[i] = bg[prob * N + i];
+    {
+        const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n_t;
+        for (int i = lane; i < n_r * n_t; i += 32) H[i] = Hp[i];
+        const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
+        for (int i = lane; i < n_r; i += 32) y[i] = yp[i];
+    }
+    double gsum = 0.0;
+    __syncwarp();
+    for (int i = 0; i < N; ++i) gsum += G[i * N + i];
+
+    // energies: lane = anneal, E = u'Gu - 2 tr G + 2 s_aux b'u  (solver.py:171-175)
+    double best_e = INFINITY;
+    int best_i = -1, ndiv = 0;
+    const int8_t* sp0 = spins + prob * (int64_t)B * S;
+    for (int a0 = 0; a0 < B; a0 += 32) {
+        const int a = a0 + lane;
+        double ea = INFINITY;
+        if (a < B) {
+            const bool dv = diverged[prob * B + a] != 0;
+            ndiv += dv;
+            if (!dv) {
+                const int8_t* s = sp0 + (int64_t)a * S;
+                double quad = 0.0, lin = 0.0;
+                for (int i = 0; i < N; ++i) {
+                    const double ui = (double)(s[i] + s[N + i]);
+                    if (ui == 0.0) continue;
+                    double gu = 0.0;
+                    for (int j = 0; j < N; ++j) gu += G[i * N + j] * (double)(s[j] + s[N + j]);
+                    quad += ui * gu;
+                    lin += b[i] * ui;
+                }
+                ea = (quad - 2.0 * gsum) + 2.0 * (double)s[2 * N] * lin;
+            }
+        }
+        if (ea < best_e) {  // strict: earlier (lower) index wins ties
+            best_e = ea;
+            best_i = a;
+        }
+    }
+    // warp argmin, ties -> lowest anneal index
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oe = __shfl_xor_sync(kFull, best_e, o);
+        const int oi = __shfl_xor_sync(kFull, best_i, o);
+        if (oe < best_e || (oe == best_e && oi >= 0 && (best_i < 0 || oi < best_i))) {
+            best_e = oe;
+            best_i = oi;
+        }
+    }
+    ndiv = __reduce_add_sync(kFull, ndiv);
+    if (diverged_count && lane == 0) diverged_count[prob] = ndiv;
+    if (!(best_e < INFINITY)) best_i = -1;
+
+    uint8_t* idx = x_idx + prob * 2 * n_t;
+    const double e_guess = energy[prob];
+    bool take = false;
+    double e_dec = 0.0;
+    __shared__ uint8_t cand_all[8][128];
+    uint8_t* cand = cand_all[warp];
+    if (best_i >= 0 && !(best_e + offset[prob] > e_guess)) {
+        const int8_t* s = sp0 + (int64_t)best_i * S;
+        const int aux = s[2 * N];
+        for (int k = lane; k < N; k += 32) {
+            const int u = s[k] + s[N + k];  // -2, 0, 2
+            const int user = k % n_t, part = k / n_t;  // k < n_t: real part
+            int v = (int)idx[2 * user + part] + aux * (u / 2);
+            v = v < 0 ? 0 : (v > al.m - 1 ? al.m - 1 : v);
+            cand[2 * user + part] = (uint8_t)v;
+        }
+        __syncwarp();
+        // residual of the decoded vector (linear.py:44-47)
+        double acc = 0.0;
+        for (int k = lane; k < n_r; k += 32) {
+            cplx sacc = {0.0, 0.0};
+            for (int j = 0; j < n_t; ++j) {
+                const cplx xj = {al.levels[cand[2 * j]], al.levels[cand[2 * j + 1]]};
+                sacc = cadd(sacc, cmul(H[k * n_t + j], xj));
+            }
+            acc += cabs2(csub(y[k], sacc));
+        }
+        e_dec = warp_sum(acc);
+        take = e_dec < e_guess;
+    }
+    if (take) {
+        for (int k = lane; k < 2 * n_t; k += 32) idx[k] = cand[k];
+        if (lane == 0) {
+            energy[prob] = e_dec;
+            if (source) source[prob] = IL_SRC_ANNEAL;
+            if (anneal_index) anneal_index[prob] = best_i;
+        }
+    } else if (lane == 0) {
+        if (source && source[prob] != IL_SRC_FAILED) source[prob] = IL_SRC_GUESS;
+        if (anneal_index) anneal_index[prob] = -1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// ZF / VPP front-end (precoder.py:54-60, 93-125)
+// ---------------------------------------------------------------------------
+__global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __restrict__ ug,
+                               int64_t P, int n_u, int n_ant, double tau, double* __restrict__ Wg,
+                               double* __restrict__ ytg, double* __restrict__ Hpg,
+                               double* __restrict__ base_energy, int8_t* __restrict__ status) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (prob >= P) return;
+    const size_t per_warp = sizeof(cplx) * ((size_t)n_u * n_ant * 2 + (size_t)n_u * n_u + n_u);
+    cplx* H = reinterpret_cast<cplx*>(smem_raw + warp * per_warp);  // [n_u x n_ant]
+    cplx* X = H + n_u * n_ant;                                      // [n_u x n_ant]
+    cplx* L = X + n_u * n_ant;                                      // [n_u x n_u]
+    cplx* u = L + n_u * n_u;
+    const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_u * n_ant;
+    for (int i = lane; i < n_u * n_ant; i += 32) H[i] = X[i] = Hp[i];
+    for (int i = lane; i < n_u; i += 32) u[i] = reinterpret_cast<const cplx*>(ug)[prob * n_u + i];
+    __syncwarp();
+    // A = H H^H  (row i of H against row j)
+    for (int idx = lane; idx < n_u * n_u; idx += 32) {
+        const int i = idx / n_u, j = idx % n_u;
+        if (i > j) continue;
+        double re = 0.0, im = 0.0;
+        for (int k = 0; k < n_ant; ++k) {
+            const cplx a = H[i * n_ant + k], bb = H[j * n_ant + k];
+            re += a.re * bb.re + a.im * bb.im;
+            im += a.im * bb.re - a.re * bb.im;
+        }
+        if (i == j) im = 0.0;
+        L[i * n_u + j] = {re, im};
+        L[j * n_u + i] = {re, -im};
+    }
+    __syncwarp();
+    const bool ok = cholesky_lower(L, n_u, lane);
+    if (lane == 0 && status) status[prob] = ok ? 0 : -1;
+    // X = A^-1 H, one column per lane
+    for (int col = lane; col < n_ant; col += 32) {
+        if (!ok) break;
+        for (int k = 0; k < n_u; ++k) {
+            const double lkk = L[k * n_u + k].re;
+            cplx acc = X[k * n_ant + col];
+            for (int j = 0; j < k; ++j) acc = csub(acc, cmul(L[k * n_u + j], X[j * n_ant + col]));
+            X[k * n_ant + col] = {acc.re / lkk, acc.im / lkk};
+        }
+        for (int k = n_u - 1; k >= 0; --k) {
+            const double lkk = L[k * n_u + k].re;
+            cplx acc = X[k * n_ant + col];
+            for (int j = k + 1; j < n_u; ++j) acc = csub(acc, cmulc(L[j * n_u + k], X[j * n_ant + col]));
+            X[k * n_ant + col] = {acc.re / lkk, acc.im / lkk};
+        }
+    }
+    __syncwarp();
+    // W = X^H [n_ant x n_u]; y_t = W u; H_p = -tau/2 W
+    cplx* W = reinterpret_cast<cplx*>(Wg) + prob * (int64_t)n_ant * n_u;
+    cplx* Hq = reinterpret_cast<cplx*>(Hpg) + prob * (int64_t)n_ant * n_u;
+    const double ht = -tau / 2.0;
+    for (int idx = lane; idx < n_ant * n_u; idx += 32) {
+        const int a = idx / n_u, i = idx % n_u;
+        const cplx xv = X[i * n_ant + a];
+        const cplx wv = {xv.re, -xv.im};
+        W[idx] = wv;
+        Hq[idx] = {ht * wv.re, ht * wv.im};
+    }
+    double acc = 0.0;
+    cplx* yt = reinterpret_cast<cplx*>(ytg) + prob * (int64_t)n_ant;
+    for (int a = lane; a < n_ant; a += 32) {
+        cplx s = {0.0, 0.0};
+        for (int i = 0; i < n_u; ++i) {
+            const cplx xv = X[i * n_ant + a];
+            s = cadd(s, cmul(cplx{xv.re, -xv.im}, u[i]));
+        }
+        yt[a] = s;
+        acc += cabs2(s);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) base_energy[prob] = acc;
+}
+
+// VPP epilogue (precoder.py:126-146).
+__global__ void k_vpp_post(const double* __restrict__ Wg, const double* __restrict__ ug,
+                           const double* __restrict__ ytg, const double* __restrict__ base_energy,
+                           const uint8_t* __restrict__ vidx, int64_t P, int n_u, int n_ant,
+                           int reach, double tau, double sqrtP, double* __restrict__ xg,
+                           double* __restrict__ vg, double* __restrict__ powg) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (prob >= P) return;
+    const cplx* W = reinterpret_cast<const cplx*>(Wg) + prob * (int64_t)n_ant * n_u;
+    const cplx* u = reinterpret_cast<const cplx*>(ug) + prob * (int64_t)n_u;
+    const cplx* yt = reinterpret_cast<const cplx*>(ytg) + prob * (int64_t)n_ant;
+    const uint8_t* vi = vidx + prob * 2 * n_u;
+    cplx* v = reinterpret_cast<cplx*>(vg) + prob * (int64_t)n_u;
+    cplx* x = reinterpret_cast<cplx*>(xg) + prob * (int64_t)n_ant;
+    // perturbed = W (u + tau v), v = vhat / 2, vhat = 4 (idx - reach)
+    double acc = 0.0;
+    cplx pk[2] = {{0, 0}, {0, 0}};
+    for (int a = lane, q = 0; a < n_ant; a += 32, ++q) {
+        cplx s = {0.0, 0.0};
+        for (int i = 0; i < n_u; ++i) {
+            const cplx vv = {4.0 * (double)((int)vi[2 * i] - reach) / 2.0,
+                             4.0 * (double)((int)vi[2 * i + 1] - reach) / 2.0};
+            const cplx t = {u[i].re + tau * vv.re, u[i].im + tau * vv.im};
+            s = cadd(s, cmul(W[a * n_u + i], t));
+        }
+        pk[q] = s;
+        acc += cabs2(s);
+    }
+    double power = warp_sum(acc);
+    const double base = base_energy[prob];
+    const bool reject = power > base;
+    if (reject) power = base;
+    for (int i = lane; i < n_u; i += 32) {
+        v[i] = reject ? cplx{0.0, 0.0}
+                      : cplx{4.0 * (double)((int)vi[2 * i] - reach) / 2.0,
+                             4.0 * (double)((int)vi[2 * i + 1] - reach) / 2.0};
+    }
+    const double nrm = sqrt(power);
+    for (int a = lane, q = 0; a < n_ant; a += 32, ++q) {
+        const cplx pa = reject ? yt[a] : pk[q];
+        x[a] = nrm == 0.0 ? cplx{0.0, 0.0} : cplx{sqrtP * pa.re / nrm, sqrtP * pa.im / nrm};
+    }
+    if (lane == 0) powg[prob] = power;
+}
+
+__global__ void k_base_seeds(const uint64_t* __restrict__ seed, int64_t P, uint64_t k1, uint64_t k2,
+                             uint64_t* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < P) out[i] = derive_seed3(seed[i], k1, k2);
+}
+
+__global__ void k_add_i32(const int32_t* __restrict__ a, int64_t n, int32_t* __restrict__ acc) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) acc[i] += a[i];
+}
+
+}  // namespace
+
+int launch_add_i32(const int32_t* a, int64_t n, int32_t* acc, cudaStream_t st) {
+    if (n == 0) return IL_OK;
+    k_add_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, n, acc);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static int set_smem(const void* fn, size_t smem) {
+    IL_REQUIRE(smem <= 227 * 1024, "per-problem matrices too large for shared memory (%zu B)", smem);
+    IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return IL_OK;
+}
+
+int launch_mmse(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
+                int n_t, const Alphabet& al, uint8_t* x_idx, double* energy, int8_t* status,
+                cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    int wpb;
+    size_t smem;
+    const int blocks = front_blocks(P, FrontSmem::bytes(n_r, n_t), &wpb, &smem);
+    int rc = set_smem((const void*)k_front<true, false>, smem);
+    if (rc) return rc;
+    IsingOut o{};
+    k_front<true, false><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
+                                                          energy, status, o);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int launch_build_ising(const double* H, const double* y, const uint8_t* guess_idx, int64_t P,
+                       int n_r, int n_t, const Alphabet& al, double* G, double* g_diag,
+                       double* b, double* offset, double* eps_scale, double* eps_out,
+                       double eps_gain, double fixed_eps, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    int wpb;
+    size_t smem;
+    const int blocks = front_blocks(P, FrontSmem::bytes(n_r, n_t), &wpb, &smem);
+    int rc = set_smem((const void*)k_front<false, true>, smem);
+    if (rc) return rc;
+    IsingOut o{G, g_diag, b, offset, eps_scale, eps_out, eps_gain, fixed_eps};
+    k_front<false, true><<<blocks, 32 * wpb, smem, st>>>(H, y, nullptr, P, n_r, n_t, al,
+                                                          const_cast<uint8_t*>(guess_idx),
+                                                          nullptr, nullptr, o);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int launch_mmse_ising(const double* H, const double* y, const double* noise_var, int64_t P,
+                      int n_r, int n_t, const Alphabet& al, uint8_t* x_idx, double* energy,
+                      int8_t* status, double* G, double* g_diag, double* b, double* offset,
+                      double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    int wpb;
+    size_t smem;
+    const int blocks = front_blocks(P, FrontSmem::bytes(n_r, n_t), &wpb, &smem);
+    int rc = set_smem((const void*)k_front<true, true>, smem);
+    if (rc) return rc;
+    IsingOut o{G, g_diag, b, offset, nullptr, eps_out, eps_gain, fixed_eps};
+    k_front<true, true><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
+                                                         energy, status, o);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int launch_select_decode(const double* H, const double* y, const double* G, const double* b,
+                         const double* offset, const int8_t* spins, const uint8_t* diverged,
+                         int64_t P, int n_r, int n_t, int B, const Alphabet& al,
+                         uint8_t* x_idx_io, double* energy_io, int8_t* source,
+                         int32_t* anneal_index, int32_t* diverged_count, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    const int N = 2 * n_t;
+    IL_REQUIRE(2 * n_t <= 128, "n_t too large");
+    const size_t per_warp =
+        ((sizeof(double) * ((size_t)N * N + N) + sizeof(cplx) * ((size_t)n_r * n_t + n_r)) + 15) / 16 * 16;
+    int wpb = (int)((200 * 1024) / per_warp);
+    wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
+    const size_t smem = per_warp * wpb;
+    int rc = set_smem((const void*)k_select_decode, smem);
+    if (rc) return rc;
+    const int blocks = (int)((P + wpb - 1) / wpb);
+    k_select_decode<<<blocks, 32 * wpb, smem, st>>>(H, y, G, b, offset, spins, diverged, P, n_r,
+                                                    n_t, B, al, x_idx_io, energy_io, source,
+                                                    anneal_index, diverged_count);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, int n_ant,
+                        double tau, double* W, double* y_t, double* H_p, double* base_energy,
+                        int8_t* status, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    const size_t per_warp = sizeof(cplx) * ((size_t)n_u * n_ant * 2 + (size_t)n_u * n_u + n_u);
+    int wpb = (int)((200 * 1024) / per_warp);
+    wpb = wpb < 1 ? 1 : (wpb > 4 ? 4 : wpb);
+    const size_t smem = per_warp * wpb;
+    int rc = set_smem((const void*)k_zf_vpp_front, smem);
+    if (rc) return rc;
+    const int blocks = (int)((P + wpb - 1) / wpb);
+    k_zf_vpp_front<<<blocks, 32 * wpb, smem, st>>>(H, u, P, n_u, n_ant, tau, W, y_t, H_p,
+                                                   base_energy, status);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int launch_vpp_post(const double* W, const double* u, const double* y_t, const double* base_energy,
+                    const uint8_t* vidx, int64_t P, int n_u, int n_ant, int reach, double tau,
+                    double power, double* x, double* v, double* unnorm_power, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    IL_REQUIRE(n_ant <= 64, "n_ant > 64 not supported");
+    const int wpb = 4;
+    const int blocks = (int)((P + wpb - 1) / wpb);
+    k_vpp_post<<<blocks, 32 * wpb, 0, st>>>(W, u, y_t, base_energy, vidx, P, n_u, n_ant, reach,
+                                            tau, sqrt(power), x, v, unnorm_power);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int launch_base_seeds(const uint64_t* seed, int64_t P, uint64_t k1, uint64_t k2,
+                      uint64_t* base_out, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    k_base_seeds<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(seed, P, k1, k2, base_out);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+}  // namespace il
+
+// ---------------------------------------------------------------------------
+// Gray demapper (channel.py:160-180): per PAM dimension label = idx ^ (idx >> 1)
+// ---------------------------------------------------------------------------
+namespace il {
+namespace {
+__global__ void k_gray_demap(const uint8_t* __restrict__ x_idx, int64_t n_dims, int bpd,
+                             uint8_t* __restrict__ bits) {
+    const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= n_dims) return;
+    const unsigned k = x_idx[d];
+    const unsigned gl = k ^ (k >> 1);
+    for (int q = 0; q < bpd; ++q) bits[d * bpd + q] = (uint8_t)((gl >> (bpd - 1 - q)) & 1u);
+}
+}  // namespace
+
+int launch_gray_demap(const uint8_t* x_idx, int64_t n_sym, int bits_per_dim, uint8_t* bits,
+                      cudaStream_t st) {
+    IL_REQUIRE(bits_per_dim >= 1 && bits_per_dim <= 8, "bits_per_dim must be in [1, 8]");
+    const int64_t n = 2 * n_sym;
+    if (n == 0) return IL_OK;
+    k_gray_demap<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x_idx, n, bits_per_dim, bits);
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+}  // namespace il

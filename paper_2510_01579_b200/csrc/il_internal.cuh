@@ -1,0 +1,96 @@
+// Internal launch interfaces shared by the .cu translation units.
+#pragma once
+#include "il_common.cuh"
+
+namespace il {
+
+// Scalars of one anneal batch (CacParams after eps resolution).
+struct AnnealScalars {
+    double p, a, zeta, eps, dt, e_floor, thr;
+    double x0_lo, x0_range;  // uniform(lo, lo + range): lo = -amp, range = amp - (-amp)
+    int f_mvm, n_steps;
+};
+
+// ---- anneal kernels --------------------------------------------------------
+// Exact FP64 (bit-identical to _kernel.pyx).  x0 == nullptr => generate from
+// base_seed[p] (anneal r seeded with derive_seed(base_seed[p], r)).
+// eps_p == nullptr => s.eps for every problem.
+int launch_anneal_exact(const double* G, const double* g, const double* b, const double* x0,
+                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
+                        const AnnealScalars& s, int8_t* spins, uint8_t* diverged,
+                        int64_t* steps, int64_t* mvms, cudaStream_t st);
+
+// FP32 state + tensor-core coupling product.  Requires N % 8 == 0 (N <= 64),
+// B % 16 == 0.  Divergence is a sticky flag (spins of diverged anneals are
+// not frozen: they never enter selection).  Returns IL_ERR_UNSUPPORTED when
+// the shape is not instantiated.
+int launch_anneal_fast(const double* G, const double* g, const double* b,
+                       const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
+                       const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
+                       cudaStream_t st);
+bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
+
+// ---- front-end / reduction kernels -----------------------------------------
+int launch_mmse(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
+                int n_t, const Alphabet& al, uint8_t* x_idx, double* energy, int8_t* status,
+                cudaStream_t st);
+// Ising around a level-index guess; eps_out[p] = eps_gain * eps_scale (or
+// fixed_eps if > 0); guess_energy (optional) = ||y - H x_guess||^2.
+int launch_build_ising(const double* H, const double* y, const uint8_t* guess_idx, int64_t P,
+                       int n_r, int n_t, const Alphabet& al, double* G, double* g_diag,
+                       double* b, double* offset, double* eps_scale, double* eps_out,
+                       double eps_gain, double fixed_eps, cudaStream_t st);
+// VPP front-end: W = H^H (H H^H)^-1 [n_ant x n_u], y_t = W u, H_p = -tau/2 W,
+// base energy ||y_t||^2.  status[p] = -1 on Cholesky breakdown.
+int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, int n_ant,
+                        double tau, double* W, double* y_t, double* H_p, double* base_energy,
+                        int8_t* status, cudaStream_t st);
+
+// ---- selection / decode -----------------------------------------------------
+// For each problem: energies of the B anneals (FP64), argmin over survivors
+// (ties -> lowest index), fallback test best+offset > guess_energy, decode
+// clamp(k_g + s_aux*(s_A+s_B)/2), residual of the decoded vector and the
+// strict improvement test (solver.py:256-279, detector.py:48-54).
+// x_idx_io holds the guess on entry and the result on exit.
+int launch_select_decode(const double* H, const double* y, const double* G, const double* b,
+                         const double* offset, const int8_t* spins, const uint8_t* diverged,
+                         int64_t P, int n_r, int n_t, int B, const Alphabet& al,
+                         uint8_t* x_idx_io, double* energy_io, int8_t* source,
+                         int32_t* anneal_index, int32_t* diverged_count, cudaStream_t st);
+
+int launch_mmse_ising(const double* H, const double* y, const double* noise_var, int64_t P,
+                      int n_r, int n_t, const Alphabet& al, uint8_t* x_idx, double* energy,
+                      int8_t* status, double* G, double* g_diag, double* b, double* offset,
+                      double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st);
+int launch_vpp_post(const double* W, const double* u, const double* y_t, const double* base_energy,
+                    const uint8_t* vidx, int64_t P, int n_u, int n_ant, int reach, double tau,
+                    double power, double* x, double* v, double* unnorm_power, cudaStream_t st);
+int launch_add_i32(const int32_t* a, int64_t n, int32_t* acc, cudaStream_t st);
+int launch_gray_demap(const uint8_t* x_idx, int64_t n_sym, int bits_per_dim, uint8_t* bits,
+                      cudaStream_t st);
+
+int launch_base_seeds(const uint64_t* seed, int64_t P, uint64_t k1, uint64_t k2,
+                      uint64_t* base_out, cudaStream_t st);
+
+// ---- workspace (stream-ordered pool allocations) ----------------------------
+struct Workspace {
+    cudaStream_t st;
+    void* ptrs[32];
+    int n = 0;
+    explicit Workspace(cudaStream_t s) : st(s) {}
+    ~Workspace();
+    template <class T>
+    T* get(size_t count, int* rc) {
+        if (*rc != IL_OK) return nullptr;
+        void* p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, count ? count * sizeof(T) : 1, st);
+        if (e != cudaSuccess) {
+            *rc = fail_cuda(e, "cudaMallocAsync(workspace)");
+            return nullptr;
+        }
+        ptrs[n++] = p;
+        return static_cast<T*>(p);
+    }
+};
+
+}  // namespace il

@@ -1,0 +1,47 @@
+"""The C-ABI library loads on CPU and exports every symbol include/*.h declares."""
+
+import glob
+import os
+import re
+import subprocess
+
+from conftest import ROOT
+
+
+def _declared():
+    names = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        text = open(h).read()
+        names |= set(re.findall(r"^\s*(?:const\s+)?\w[\w\s\*]*?\b(il_\w+)\s*\(", text, re.M))
+    return names
+
+
+def test_header_declares_entry_points():
+    names = _declared()
+    for must in ("il_run_anneals", "il_run_anneals_host", "il_detect_cim_batch",
+                 "il_precode_vpp_batch", "il_last_error", "il_gray_demap"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(built_lib):
+    from paper_2510_01579_b200 import _lib
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r"\bT (il_\w+)", out))
+    missing = _declared() - exported
+    assert not missing, missing
+    assert set(_lib.EXPORTED) <= exported
+
+
+def test_library_loads_without_gpu(built_lib):
+    from paper_2510_01579_b200 import _lib
+    lib = _lib.load()
+    assert lib.il_abi_version() == 1
+    assert isinstance(lib.il_last_error(), bytes)
+
+
+def test_cubin_is_sm100a(built_lib):
+    from paper_2510_01579_b200 import _lib
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
