@@ -1,0 +1,423 @@
+"""Benchmark: MIMO detections/sec and per-slot latency (16x16 16-QAM, 273 PRB).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the hot path over one full 100 MHz / 30 kHz slot
+(273 PRB x 12 subcarriers x 14 symbols = 45,864 resource elements), each RE a
+16x16 16-QAM uplink detection at 20 dB (BASELINE.json configs[2], the
+configuration the headline metric is quoted on).  Under torchrun the slot is
+sharded by subcarrier range across ranks (strong scaling) and the detected
+Gray bits are gathered to rank 0 with one NCCL all_gather.
+
+Inputs are synthetic i.i.d. Rayleigh channels generated on the device (the
+full slot is generated identically on every rank and sliced, so outputs do
+not depend on the GPU count); they total 188 MB > the 126 MB L2, so no L2
+flush is needed between steps.  ``value`` is device-resident throughput;
+``e2e`` runs the same public batch API from pinned host buffers with the
+H2D copy of the step's inputs and the D2H copy of its decisions inside the
+timed region.
+
+``--impl reference`` times the reference CPU path (the compiled reference
+kernel from oracle/_ref when present, else the C oracle, inside the oracle's
+restatement of detect_cim) on all host cores, on bounded samples of the same
+workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+os.environ.setdefault("OMP_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MIMO detections/sec (16x16 16-QAM, 273 PRB slot, BER parity)"
+UNIT = "detections/s"
+N_R = N_T = 16
+ORDER = 16
+SNR_DB = 20.0
+N_PRB = 273
+MASTER_SEED = 1
+
+
+def flop_model(n_t: int, n_anneals: int, n_steps: int, f_mvm: int):
+    """algorithmic FP32 flops per detection, split into the
+    coupling product (tensor cores here) and the rest (FP32 pipe)."""
+    N = 2 * n_t
+    S = 2 * N + 1
+    refresh = math.ceil(n_steps / f_mvm)
+    mvm = refresh * 2 * N * N
+    ew = refresh * 11 * N + 14 * n_steps * S + (2 * N * N + 5 * N)
+    return n_anneals * (mvm + ew), n_anneals * mvm, n_anneals * ew
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        if self.thread:
+            self.thread.join(timeout=5)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle) — bounded samples on all host cores
+# ---------------------------------------------------------------------------
+_CPU_CTX = {}
+
+
+def _cpu_worker(args):
+    H, y, s2, seed = args
+    orc = _CPU_CTX["orc"]
+    kernel = _CPU_CTX["kernel"]
+    r = orc.detect_cim(H, y, float(s2), ORDER, seed=int(seed), kernel=kernel)
+    return r["energy"]
+
+
+def _cpu_init():
+    from oracle import isinglink_oracle as orc
+    _CPU_CTX["orc"] = orc
+    ref = orc.ref_kernel_module()
+    _CPU_CTX["kernel"] = ref.run_anneals if ref is not None else None
+
+
+def cpu_instances(n: int, seed: int = 7):
+    rng = np.random.default_rng(seed)
+    H = (rng.standard_normal((n, N_R, N_T)) + 1j * rng.standard_normal((n, N_R, N_T))) * np.sqrt(0.5)
+    m = int(math.isqrt(ORDER))
+    lv = np.arange(-(m - 1), m, 2) / math.sqrt(2 * (m * m - 1) / 3)
+    x = lv[rng.integers(0, m, (n, N_T))] + 1j * lv[rng.integers(0, m, (n, N_T))]
+    s2 = N_T / 10 ** (SNR_DB / 10)
+    y = np.einsum("prt,pt->pr", H, x) + (rng.standard_normal((n, N_R)) + 1j * rng.standard_normal(
+        (n, N_R))) * math.sqrt(s2 / 2)
+    seeds = rng.integers(0, 2**63, n, dtype=np.uint64)
+    return [(H[i], y[i], s2, int(seeds[i])) for i in range(n)]
+
+
+def cpu_rate(n_res: int, cores: int, pool=None):
+    """Detections/s of the CPU reference path on `n_res` fresh instances."""
+    import multiprocessing as mp
+    inst = cpu_instances(n_res)
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init)
+        pool.map(_cpu_worker, inst[:cores], chunksize=1)  # warm the workers
+    t0 = time.perf_counter()
+    pool.map(_cpu_worker, inst, chunksize=max(1, n_res // (cores * 4)))
+    dt = time.perf_counter() - t0
+    if own:
+        pool.close()
+        pool.join()
+    return n_res / dt, dt
+
+
+def cpu_kind() -> str:
+    from oracle import isinglink_oracle as orc
+    return "reference" if orc.ref_kernel_module() is not None else "port"
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = host_cores()
+    kind = cpu_kind()
+    per_step = max(cores * 4, 64)
+    pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init)
+    pool.map(_cpu_worker, cpu_instances(cores), chunksize=1)
+    for _ in range(args.warmup):
+        cpu_rate(per_step, cores, pool)
+    rates, times = [], []
+    for _ in range(args.steps):
+        r, dt = cpu_rate(per_step, cores, pool)
+        rates.append(r)
+        times.append(dt)
+    pool.close()
+    pool.join()
+    total = per_step * args.steps
+    value = total / sum(times)
+    sample = (f"{per_step} fresh 16x16 16-QAM 20 dB REs per step on {cores} host processes; "
+              + ("reference Cython kernel (oracle/_ref) inside the oracle's detect_cim glue"
+                 if kind == "reference" else "C oracle kernel inside the oracle's detect_cim glue"))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(times) / args.steps,
+        "slot_latency_ms_extrapolated": 1e3 * (N_PRB * 12 * 14) / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": workload_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args) -> dict:
+    return {"workload": "16x16 16-QAM uplink full slot (273 PRB x 12 sc x 14 sym = 45864 REs), "
+                        "i.i.d. Rayleigh, 20 dB",
+            "n_r": N_R, "n_t": N_T, "qam": ORDER, "snr_db": SNR_DB, "n_prb": N_PRB,
+            "res_per_step": N_PRB * 12 * 14, "n_anneals": 32, "n_steps": 128, "f_mvm": 2,
+            "dt": 0.02, "precision": args.precision, "parallelism": f"subcarrier-shard x{args.gpus}",
+            "l2": "inputs 188 MB > 126 MB L2 (no flush needed)"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_01579_b200 import _lib, batched
+    from paper_2510_01579_b200.params import CacParams
+    from paper_2510_01579_b200.shard import gather_to_rank0, slot_shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    _lib.load()
+    shard = slot_shard(N_PRB, rank, world)
+    P_all = shard.n_res
+    lo, hi = shard.re_start, shard.re_stop
+    P = hi - lo
+
+    # ---- synthetic slot (identical on every rank), sliced to the shard ----
+    gen = torch.Generator(device=dev).manual_seed(MASTER_SEED)
+    H = torch.complex(torch.randn(P_all, N_R, N_T, dtype=torch.float64, device=dev, generator=gen),
+                      torch.randn(P_all, N_R, N_T, dtype=torch.float64, device=dev, generator=gen))
+    H *= math.sqrt(0.5)
+    m = int(math.isqrt(ORDER))
+    levels = (torch.arange(-(m - 1), m, 2, dtype=torch.float64, device=dev)
+              / math.sqrt(2 * (m * m - 1) / 3))
+    sym_re = torch.randint(0, m, (P_all, N_T), device=dev, generator=gen)
+    sym_im = torch.randint(0, m, (P_all, N_T), device=dev, generator=gen)
+    x = torch.complex(levels[sym_re], levels[sym_im])
+    s2 = N_T / 10 ** (SNR_DB / 10)
+    noise = torch.complex(torch.randn(P_all, N_R, dtype=torch.float64, device=dev, generator=gen),
+                          torch.randn(P_all, N_R, dtype=torch.float64, device=dev, generator=gen))
+    y = torch.einsum("prt,pt->pr", H, x) + noise * math.sqrt(s2 / 2)
+    nv = torch.full((P_all,), s2, dtype=torch.float64, device=dev)
+    parts = np.stack([np.full(P_all, MASTER_SEED), np.full(P_all, 1), np.zeros(P_all),
+                      np.arange(P_all), np.full(P_all, 3)], axis=1).astype(np.uint64)
+    seeds = batched.derive_seeds(parts)  # detector seed of RE t: derive_seed(seed, 1, 0, t, 3)
+    H, y, nv, seeds = (H[lo:hi].contiguous(), y[lo:hi].contiguous(), nv[lo:hi].contiguous(),
+                       seeds[lo:hi].contiguous())
+    truth = torch.stack([sym_re[lo:hi], sym_im[lo:hi]], -1).to(torch.uint8)
+    del x, noise, sym_re, sym_im
+    prm = CacParams(precision=args.precision)
+    bpd = int(round(math.log2(m)))
+
+    def step():
+        r = batched.detect_cim_batch(H, y, nv, ORDER, seeds, prm)
+        if world > 1:
+            bits = batched.gray_demap(r.x_idx, bpd)
+            gather_to_rank0(bits, shard)
+        return r
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        res = step()
+    barrier()
+    ser = (res.x_idx != truth).any(-1).float().mean().item()
+
+    # ---- timed region: device-resident ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    stream = torch.cuda.current_stream()
+    l0 = _lib.kernel_launches()
+    _lib.profile_begin()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    barrier()
+    prof = _lib.profile_end()
+    launches = _lib.kernel_launches() - l0
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = P_all * args.steps / (ms_max / 1e3)
+
+    # ---- e2e: pinned host buffers, H2D + detect + D2H inside the region ----
+    Hh = H.cpu().pin_memory()
+    yh = y.cpu().pin_memory()
+    nvh = nv.cpu().pin_memory()
+    sh = seeds.cpu().pin_memory()
+    out_h = torch.empty((P, N_T, 2), dtype=torch.uint8).pin_memory()
+    h2d = Hh.numel() * 16 + yh.numel() * 16 + nvh.numel() * 8 + sh.numel() * 8
+    d2h = out_h.numel()
+
+    def e2e_step():
+        Hd = Hh.to(dev, non_blocking=True)
+        yd = yh.to(dev, non_blocking=True)
+        nd = nvh.to(dev, non_blocking=True)
+        sd = sh.to(dev, non_blocking=True)
+        r = batched.detect_cim_batch(Hd, yd, nd, ORDER, sd, prm)
+        if world > 1:
+            gather_to_rank0(batched.gray_demap(r.x_idx, bpd), shard)
+        out_h.copy_(r.x_idx, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    e2e_step()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    barrier()
+    e2e_ms = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = P_all * args.steps / (float(e2e_ms.item()) / 1e3)
+
+    # ---- roofline of the dominant kernel (anneal), from live CUDA events ----
+    f_det, f_mvm, f_ew = flop_model(N_T, prm.n_anneals, prm.n_steps, prm.f_mvm)
+    an_ms, an_n = prof["anneal"]
+    fp32_peak = _lib.fp32_peak_tflops(5)
+    per_launch_s = (an_ms / max(an_n, 1)) / 1e3
+    achieved = f_ew * P / per_launch_s / 1e12 if an_n else None
+    mvm_tf = f_mvm * P / per_launch_s / 1e12 if an_n else None
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cores = host_cores()
+        n_cpu = max(cores * 8, 64)
+        rate, dt = cpu_rate(n_cpu, cores)
+        if dt < 5.0:  # grow the sample toward ~10-30 s of CPU work
+            n_cpu = int(n_cpu * min(12.0 / max(dt, 1e-3), 200))
+            rate, dt = cpu_rate(n_cpu, cores)
+        kind = cpu_kind()
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": f"{n_cpu} fresh 16x16 16-QAM 20 dB REs on {cores} host processes "
+                         f"({dt:.1f} s); " + ("reference Cython kernel (oracle/_ref)" if kind ==
+                                                "reference" else "C oracle kernel")
+                         + " inside the oracle's detect_cim"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "slot_latency_ms": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": workload_config(args),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "fp32", "kernel": "k_anneal_fast",
+                     "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                     "frac": (achieved / fp32_peak) if achieved else None,
+                     "peak_source": "measured FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
+                     "flops_per_detection_fp32_pipe": f_ew, "flops_per_detection_mvm_tensor": f_mvm,
+                     "mvm_tflops_on_tensor_cores": mvm_tf,
+                     "anneal_ms_per_launch": an_ms / max(an_n, 1),
+                     "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+                     "traffic": None},
+        "clocks": clk,
+        "ser_check": ser,
+    }
+    if cpu is not None:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "tf32", "fp64_exact"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

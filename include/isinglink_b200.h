@@ -154,6 +154,20 @@ int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_
 int il_gray_demap(const uint8_t* x_idx, int64_t n_sym, int32_t bits_per_dim,
                   uint8_t* bits, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Measurement hooks (no reference counterpart; used by bench.py).
+ *   il_kernel_launches: cumulative number of kernels this library launched.
+ *   il_profile_begin/end: while enabled, every launch is bracketed by CUDA
+ *     events on its stream; il_profile_end synchronises and returns summed
+ *     milliseconds and launch counts per kind (0 front-end/reduction,
+ *     1 anneal, 2 select/decode, 3 other), n_kinds <= 4.
+ *   il_probe_fp32_peak: dense FFMA throughput (TFLOP/s) of the current GPU.
+ * ------------------------------------------------------------------------- */
+long long il_kernel_launches(void);
+void il_profile_begin(void);
+int il_profile_end(double* ms_by_kind, long long* launches_by_kind, int n_kinds);
+int il_probe_fp32_peak(int reps, double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

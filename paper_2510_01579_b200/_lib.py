@@ -51,6 +51,10 @@ _SIGS = {
                               ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp],
                              ctypes.c_int),
     "il_gray_demap": ([_vp, _c_i64, _c_i32, _vp, _vp], ctypes.c_int),
+    "il_kernel_launches": ([], ctypes.c_longlong),
+    "il_profile_begin": ([], None),
+    "il_profile_end": ([_vp, _vp, ctypes.c_int], ctypes.c_int),
+    "il_probe_fp32_peak": ([ctypes.c_int, _vp], ctypes.c_int),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -93,3 +97,29 @@ def check(rc: int) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args))
+
+
+PROFILE_KINDS = ("front", "anneal", "select", "other")
+
+
+def profile_begin() -> None:
+    load().il_profile_begin()
+
+
+def profile_end() -> dict:
+    """{kind: (milliseconds, launches)} summed over the profiled region."""
+    import numpy as np
+    ms = np.zeros(4, np.float64)
+    n = np.zeros(4, np.int64)
+    check(load().il_profile_end(ms.ctypes.data, n.ctypes.data, 4))
+    return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(PROFILE_KINDS)}
+
+
+def kernel_launches() -> int:
+    return int(load().il_kernel_launches())
+
+
+def fp32_peak_tflops(reps: int = 5) -> float:
+    out = ctypes.c_double(0.0)
+    check(load().il_probe_fp32_peak(int(reps), ctypes.addressof(out)))
+    return float(out.value)

@@ -25,6 +25,20 @@ int fail_cuda(cudaError_t e, const char* what) {
     return IL_ERR_CUDA;
 }
 
+static void keep_pool_memory() {
+    static bool done = false;
+    if (done) return;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done = true;
+}
+
+Workspace::Workspace(cudaStream_t s) : st(s) { keep_pool_memory(); }
+
 Workspace::~Workspace() {
     for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], st);
 }
@@ -113,15 +127,19 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
     uint8_t* div = ws.get<uint8_t>((size_t)P * B, &rc);
     if (rc) return rc;
     const AnnealScalars s = scalars_of(prm);
+    double* energies = nullptr;
     if (prm->precision != IL_PREC_FP64_EXACT && fast_anneal_supported(N, B, s)) {
-        rc = launch_anneal_fast(G, g, b, base, eps, P, N, B, s, prm->precision, spins, div, st);
+        energies = ws.get<double>((size_t)P * B, &rc);
+        if (rc) return rc;
+        rc = launch_anneal_fast(G, g, b, base, eps, P, N, B, s, prm->precision, spins, div,
+                                energies, st);
     } else {
         rc = launch_anneal_exact(G, g, b, nullptr, base, eps, P, N, B, s, spins, div, nullptr,
                                  nullptr, st);
     }
     if (rc) return rc;
-    return launch_select_decode(H, y, G, b, offset, spins, div, P, n_r, n_t, B, al, x_idx, energy,
-                                source, anneal_index, diverged_count, st);
+    return launch_select_decode(H, y, G, b, offset, spins, div, energies, P, n_r, n_t, B, al, x_idx,
+                                energy, source, anneal_index, diverged_count, st);
 }
 
 }  // namespace il

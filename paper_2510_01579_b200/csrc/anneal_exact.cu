@@ -146,8 +146,8 @@ int launch_anneal_exact(const double* G, const double* g, const double* b, const
     const int chunks = (B + kLanes - 1) / kLanes;
     const int64_t blocks = P * chunks;
     IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
-    k_anneal_exact<<<(unsigned)blocks, kLanes, smem, st>>>(G, g, b, x0, base_seed, eps_p, P, N, B,
-                                                           chunks, s, spins, diverged, steps, mvms);
+    IL_LAUNCH(kProfAnneal, st, k_anneal_exact<<<(unsigned)blocks, kLanes, smem, st>>>(G, g, b, x0, base_seed, eps_p, P, N, B,
+                                                           chunks, s, spins, diverged, steps, mvms););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }

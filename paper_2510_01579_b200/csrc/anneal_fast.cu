@@ -33,8 +33,6 @@
 //
 // Scaling: G, g, b are pre-multiplied by -dt*eps so that the MMA directly
 // yields the -dt*eps*c term of the update.
-#include <mma.h>
-
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
 
@@ -59,7 +57,7 @@ struct FastScalars {
 
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return r;
 }
 
@@ -88,37 +86,53 @@ __device__ __forceinline__ float max_nan(float a, float b) {
 //   x' = x (alpha - dt x^2) + e C      (C = -dt eps c)
 //   e' = max(e_floor, e (beta - dt zeta x^2))
 // x2 of the incoming state is folded into the divergence max.
+template <bool SAME_QR>
 __device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
                                            const FastScalars& s, float& dv) {
     const float2 x2 = __fmul2_rn(x, x);
     dv = max_nan3(dv, x2.x, x2.y);
     const float2 q = __ffma2_rn(make_float2(s.ndt, s.ndt), x2, make_float2(s.alpha, s.alpha));
-    const float2 r = __ffma2_rn(make_float2(s.ndtz, s.ndtz), x2, make_float2(s.beta, s.beta));
+    // at the default operating point (zeta = 1, p - 1 = a) the x and e
+    // factors coincide exactly and one packed FMA is saved
+    const float2 r = SAME_QR ? q
+                             : __ffma2_rn(make_float2(s.ndtz, s.ndtz), x2, make_float2(s.beta, s.beta));
     const float2 t = __fmul2_rn(x, q);
     x = __ffma2_rn(e, C, t);
     const float2 er = __fmul2_rn(e, r);
     e = make_float2(fmaxf(er.x, s.e_floor), fmaxf(er.y, s.e_floor));
 }
 
+template <bool SAME_QR>
 __device__ __forceinline__ void euler_one(float& x, float& e, const float C, const FastScalars& s,
                                           float& dv) {
     const float x2 = x * x;
     dv = max_nan(dv, x2);
     const float q = fmaf(s.ndt, x2, s.alpha);
-    const float r = fmaf(s.ndtz, x2, s.beta);
+    const float r = SAME_QR ? q : fmaf(s.ndtz, x2, s.beta);
     x = fmaf(e, C, x * q);
     e = fmaxf(e * r, s.e_floor);
 }
 
-template <int NT, bool SPLIT>
-__global__ void __launch_bounds__(kWarpsPerCta * 32)
+template <int NT>
+struct FastLayout {
+    static constexpr int N = 8 * NT;
+    static constexpr int S = 2 * N + 1;
+    static constexpr int kFragF4 = NT * NT * 32;          // float4 per warp
+    static constexpr int kX0F4 = (16 * S + 3) / 4;        // x0 staging, aliased
+    static constexpr int kWarpF4 = kFragF4 > kX0F4 ? kFragF4 : kX0F4;
+    static constexpr size_t kSmem = sizeof(float4) * kWarpsPerCta * kWarpF4;
+};
+
+template <int NT, bool SPLIT, bool SAME_QR>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, 3)
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
               const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
-              FastScalars s, int8_t* __restrict__ spins, uint8_t* __restrict__ diverged) {
-    constexpr int N = 8 * NT;
-    constexpr int S = 2 * N + 1;
-    // per warp: G fragments [NT][NT][32] x float4 (hi0, hi1, lo0, lo1) + x0 staging [16][S]
+              FastScalars s, int8_t* __restrict__ spins, uint8_t* __restrict__ diverged,
+              double* __restrict__ energies) {
+    using L = FastLayout<NT>;
+    constexpr int N = L::N;
+    constexpr int S = L::S;
     extern __shared__ __align__(16) float4 smem_f4[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerCta + warp;
@@ -126,12 +140,42 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     const int64_t prob = task / tiles_per_prob;
     const int mt = (int)(task % tiles_per_prob);
     const int B = tiles_per_prob * 16;
-    float4* frag = smem_f4 + warp * (NT * NT * 32 + (16 * S + 3) / 4);
-    float* x0s = reinterpret_cast<float*>(frag + NT * NT * 32);
+    float4* frag = smem_f4 + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
+    float* x0s = reinterpret_cast<float*>(frag);      // x0 staging [16][S]
 
     const int g = lane >> 2, t = lane & 3;
+    const int hown = t & 1;  // the aux spin of anneal g + 8*hown is integrated by this lane
     const double K = s.dt * eps_p[prob];
     const double* G = Gall + prob * (int64_t)N * N;
+
+    // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
+    {
+        const int al = lane & 15, part = lane >> 4;
+        const int a = mt * 16 + al;
+        Pcg64 rng;
+        rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)a));
+        constexpr int S0 = (S + 1) / 2;
+        if (part) rng.state = add128(mul128(rng.state, s.jump_mult), mul128(rng.inc, s.jump_add));
+        const int i0 = part ? S0 : 0, i1 = part ? S : S0;
+        for (int i = i0; i < i1; ++i) x0s[al * S + i] = (float)rng.uniform(s.x0_lo, s.x0_range);
+    }
+    __syncwarp();
+    float2 xA[2][NT], xB[2][NT], eA[2][NT], eB[2][NT], CA[2][NT], CB[2][NT];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const float* r = x0s + (g + 8 * h) * S;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const int i = 8 * n + 2 * t;
+            xA[h][n] = make_float2(r[i], r[i + 1]);
+            xB[h][n] = make_float2(r[N + i], r[N + i + 1]);
+            eA[h][n] = eB[h][n] = make_float2(1.f, 1.f);
+            CA[h][n] = CB[h][n] = make_float2(0.f, 0.f);
+        }
+    }
+    float xa = x0s[(g + 8 * hown) * S + 2 * N], ea = 1.f, Ca = 0.f, dva = 0.f;
+    float dv[2] = {0.f, 0.f};
+    __syncwarp();
 
     // ---- stage -K*G as permuted TF32 B fragments (hi, lo) ------------------
 #pragma unroll
@@ -155,41 +199,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         Kg[n] = make_float2((float)(K * gall[prob * N + i]), (float)(K * gall[prob * N + i + 1]));
         nKb[n] = make_float2((float)(-K * ball[prob * N + i]), (float)(-K * ball[prob * N + i + 1]));
     }
-
-    // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
-    {
-        const int al = lane & 15, part = lane >> 4;
-        const int a = mt * 16 + al;
-        Pcg64 rng;
-        rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)a));
-        constexpr int S0 = (S + 1) / 2;
-        if (part) rng.state = add128(mul128(rng.state, s.jump_mult), mul128(rng.inc, s.jump_add));
-        const int i0 = part ? S0 : 0, i1 = part ? S : S0;
-        for (int i = i0; i < i1; ++i) x0s[al * S + i] = (float)rng.uniform(s.x0_lo, s.x0_range);
-    }
     __syncwarp();
 
-    float2 xA[2][NT], xB[2][NT], eA[2][NT], eB[2][NT], CA[2][NT], CB[2][NT];
-    float xa[2], ea[2], Ca[2], dv[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const float* r = x0s + (g + 8 * h) * S;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            const int i = 8 * n + 2 * t;
-            xA[h][n] = make_float2(r[i], r[i + 1]);
-            xB[h][n] = make_float2(r[N + i], r[N + i + 1]);
-            eA[h][n] = eB[h][n] = make_float2(1.f, 1.f);
-            CA[h][n] = CB[h][n] = make_float2(0.f, 0.f);
-        }
-        xa[h] = r[2 * N];
-        ea[h] = 1.f;
-        Ca[h] = 0.f;
-        dv[h] = 0.f;
-    }
-
+    int until_refresh = 0;
     for (int step = 0; step < s.n_steps; ++step) {
-        if (step % s.f_mvm == 0) {
+        if (until_refresh == 0) {
+            until_refresh = s.f_mvm;
             // ---- refresh: v = x1 + x2, M' = -K G v on tensor cores ------------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
@@ -201,11 +216,16 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                     pb[h] = fmaf(nKb[n].x, v[h][n].x, pb[h]);
                     pb[h] = fmaf(nKb[n].y, v[h][n].y, pb[h]);
                 }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                pb[h] += __shfl_xor_sync(0xffffffffu, pb[h], 1);
-                pb[h] += __shfl_xor_sync(0xffffffffu, pb[h], 2);
-                Ca[h] = pb[h];
+            // aux states of both anneals of the quad, from their owner lanes
+            const float xa0 = __shfl_sync(0xffffffffu, xa, (lane & ~3) | 0);
+            const float xa1 = __shfl_sync(0xffffffffu, xa, (lane & ~3) | 1);
+            {
+                const float mine = hown ? pb[1] : pb[0];
+                const float other = hown ? pb[0] : pb[1];
+                // quad sum of the own anneal's partials: lanes t and t^2 share hown
+                float tot = mine + __shfl_xor_sync(0xffffffffu, other, 1);
+                tot += __shfl_xor_sync(0xffffffffu, tot, 2);
+                Ca = tot;
             }
             float acc[NT][4];
 #pragma unroll
@@ -217,7 +237,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     ahi[q] = to_tf32(av[q]);
-                    alo[q] = to_tf32(av[q] - __uint_as_float(ahi[q]));
+                    // hardware ignores the low 13 bits of a TF32 operand: the lo
+                    // part is passed unrounded (truncated), error ~2^-21 relative
+                    alo[q] = __float_as_uint(av[q] - __uint_as_float(ahi[q]));
                 }
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
@@ -231,89 +253,148 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             }
             // ---- coupling assembly: C = M' + K g x_self - K b xa -------------
 #pragma unroll
-            for (int h = 0; h < 2; ++h)
+            for (int h = 0; h < 2; ++h) {
+                const float xah = h ? xa1 : xa0;
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
                     const float2 m2 = make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
-                    const float2 u2 = __ffma2_rn(nKb[n], make_float2(xa[h], xa[h]), m2);
+                    const float2 u2 = __ffma2_rn(nKb[n], make_float2(xah, xah), m2);
                     CA[h][n] = __ffma2_rn(Kg[n], xA[h][n], u2);
                     CB[h][n] = __ffma2_rn(Kg[n], xB[h][n], u2);
                 }
+            }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-                euler_pair(xA[h][n], eA[h][n], CA[h][n], s, dv[h]);
-                euler_pair(xB[h][n], eB[h][n], CB[h][n], s, dv[h]);
+                euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, dv[h]);
+                euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, dv[h]);
             }
-            euler_one(xa[h], ea[h], Ca[h], s, dv[h]);
         }
+        euler_one<SAME_QR>(xa, ea, Ca, s, dva);
+        --until_refresh;
     }
 
-    // ---- final divergence check, spins out ---------------------------------
+    // ---- epilogue: divergence flags, spins, FP64 energies --------------------
+    // E = u'Gu - 2 tr G + 2 s_aux b'u with u = s_A + s_B (solver.py:171-175)
+    const float xa_h[2] = {__shfl_sync(0xffffffffu, xa, (lane & ~3) | 0),
+                           __shfl_sync(0xffffffffu, xa, (lane & ~3) | 1)};
+    {
+        float d = max_nan(dva, xa * xa);  // own aux: fold into dv of its anneal
+        dv[hown] = max_nan(dv[hown], d);
+    }
     const int64_t row0 = prob * (int64_t)B + mt * 16;
+    uint64_t pos[2], neg[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         float d = dv[h];
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-            d = max_nan3(d, xA[h][n].x * xA[h][n].x, xA[h][n].y * xA[h][n].y);
-            d = max_nan3(d, xB[h][n].x * xB[h][n].x, xB[h][n].y * xB[h][n].y);
-        }
-        d = max_nan(d, xa[h] * xa[h]);
-        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 1));
-        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 2));
+        uint64_t pm = 0, nm = 0;
         const int64_t row = row0 + g + 8 * h;
         int8_t* sp = spins + row * S;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
+            d = max_nan3(d, xA[h][n].x * xA[h][n].x, xA[h][n].y * xA[h][n].y);
+            d = max_nan3(d, xB[h][n].x * xB[h][n].x, xB[h][n].y * xB[h][n].y);
             const int i = 8 * n + 2 * t;
-            char2 sa, sb;
-            sa.x = xA[h][n].x >= 0.f ? 1 : -1;
-            sa.y = xA[h][n].y >= 0.f ? 1 : -1;
-            sb.x = xB[h][n].x >= 0.f ? 1 : -1;
-            sb.y = xB[h][n].y >= 0.f ? 1 : -1;
-            sp[i] = sa.x;
-            sp[i + 1] = sa.y;
-            sp[N + i] = sb.x;
-            sp[N + i + 1] = sb.y;
+            const int a0 = xA[h][n].x >= 0.f ? 1 : -1, a1 = xA[h][n].y >= 0.f ? 1 : -1;
+            const int b0 = xB[h][n].x >= 0.f ? 1 : -1, b1 = xB[h][n].y >= 0.f ? 1 : -1;
+            sp[i] = (int8_t)a0;
+            sp[i + 1] = (int8_t)a1;
+            sp[N + i] = (int8_t)b0;
+            sp[N + i + 1] = (int8_t)b1;
+            pm |= (uint64_t)(a0 + b0 == 2) << i | (uint64_t)(a1 + b1 == 2) << (i + 1);
+            nm |= (uint64_t)(a0 + b0 == -2) << i | (uint64_t)(a1 + b1 == -2) << (i + 1);
         }
-        if (t == 0) {
-            sp[2 * N] = xa[h] >= 0.f ? 1 : -1;
-            diverged[row] = (d <= s.thr2) ? 0 : 1;
+        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 1));
+        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 2));
+        pm |= __shfl_xor_sync(0xffffffffu, pm, 1);
+        pm |= __shfl_xor_sync(0xffffffffu, pm, 2);
+        nm |= __shfl_xor_sync(0xffffffffu, nm, 1);
+        nm |= __shfl_xor_sync(0xffffffffu, nm, 2);
+        pos[h] = pm;
+        neg[h] = nm;
+        if (t == h) sp[2 * N] = xa >= 0.f ? 1 : -1;
+        if (t == 0) diverged[row] = (d <= s.thr2) ? 0 : 1;
+    }
+    // partial quadratic / linear / trace terms over this lane's rows
+    const double* bg = ball + prob * N;
+    double quad[2] = {0.0, 0.0}, lin[2] = {0.0, 0.0}, tr = 0.0;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+#pragma unroll
+        for (int dl = 0; dl < 2; ++dl) {
+            const int i = 8 * n + 2 * t + dl;
+            const double* Gi = G + (int64_t)i * N;
+            double rs0 = 0.0, rs1 = 0.0;
+            for (int j = 0; j < N; j += 2) {
+                const double2 gij = __ldg(reinterpret_cast<const double2*>(Gi + j));
+                const double s00 = (double)((int)((pos[0] >> j) & 1u) - (int)((neg[0] >> j) & 1u));
+                const double s01 = (double)((int)((pos[0] >> (j + 1)) & 1u) - (int)((neg[0] >> (j + 1)) & 1u));
+                const double s10 = (double)((int)((pos[1] >> j) & 1u) - (int)((neg[1] >> j) & 1u));
+                const double s11 = (double)((int)((pos[1] >> (j + 1)) & 1u) - (int)((neg[1] >> (j + 1)) & 1u));
+                rs0 = fma(gij.x, s00, rs0);
+                rs0 = fma(gij.y, s01, rs0);
+                rs1 = fma(gij.x, s10, rs1);
+                rs1 = fma(gij.y, s11, rs1);
+            }
+            const double si0 = (double)((int)((pos[0] >> i) & 1u) - (int)((neg[0] >> i) & 1u));
+            const double si1 = (double)((int)((pos[1] >> i) & 1u) - (int)((neg[1] >> i) & 1u));
+            quad[0] = fma(si0, rs0, quad[0]);
+            quad[1] = fma(si1, rs1, quad[1]);
+            const double bi = __ldg(bg + i);
+            lin[0] = fma(bi, si0, lin[0]);
+            lin[1] = fma(bi, si1, lin[1]);
+            tr += __ldg(Gi + i);
         }
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        quad[0] += __shfl_xor_sync(0xffffffffu, quad[0], o);
+        quad[1] += __shfl_xor_sync(0xffffffffu, quad[1], o);
+        lin[0] += __shfl_xor_sync(0xffffffffu, lin[0], o);
+        lin[1] += __shfl_xor_sync(0xffffffffu, lin[1], o);
+        tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    }
+    if (t < 2) {
+        const int h = t;
+        const double aux = xa_h[h] >= 0.f ? 1.0 : -1.0;
+        energies[row0 + g + 8 * h] = (4.0 * quad[h] - 2.0 * tr) + 4.0 * aux * lin[h];
     }
 }
 
-template <int NT>
-size_t fast_smem(int) {
-    constexpr int S = 16 * NT + 1;
-    return sizeof(float4) * kWarpsPerCta * (NT * NT * 32 + (16 * S + 3) / 4);
+template <int NT, bool SPLIT, bool SAME_QR>
+int launch_cfg(const double* G, const double* g, const double* b, const uint64_t* base_seed,
+               const double* eps_p, int64_t n_tasks, int tiles, const FastScalars& fs,
+               int8_t* spins, uint8_t* diverged, double* energies, cudaStream_t st) {
+    const int64_t blocks = (n_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
+    IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
+    const size_t smem = FastLayout<NT>::kSmem;
+    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR>;
+    IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    IL_LAUNCH(kProfAnneal, st, fn<<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(G, g, b, base_seed, eps_p, n_tasks, tiles,
+                                                        fs, spins, diverged, energies););
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
 }
 
 template <int NT>
 int launch_nt(const double* G, const double* g, const double* b, const uint64_t* base_seed,
               const double* eps_p, int64_t P, int B, const FastScalars& fs, bool split,
-              int8_t* spins, uint8_t* diverged, cudaStream_t st) {
+              bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, cudaStream_t st) {
     const int tiles = B / 16;
     const int64_t n_tasks = P * tiles;
-    const int64_t blocks = (n_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
-    IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
-    const size_t smem = fast_smem<NT>(0);
     if (split) {
-        IL_CHECK_CUDA(cudaFuncSetAttribute(k_anneal_fast<NT, true>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_anneal_fast<NT, true><<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(
-            G, g, b, base_seed, eps_p, n_tasks, tiles, fs, spins, diverged);
-    } else {
-        IL_CHECK_CUDA(cudaFuncSetAttribute(k_anneal_fast<NT, false>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_anneal_fast<NT, false><<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(
-            G, g, b, base_seed, eps_p, n_tasks, tiles, fs, spins, diverged);
+        return same_qr ? launch_cfg<NT, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                   spins, diverged, energies, st)
+                       : launch_cfg<NT, true, false>(G, g, b, base_seed, eps_p, n_tasks, tiles,
+                                                    fs, spins, diverged, energies, st);
     }
-    IL_CHECK_CUDA(cudaGetLastError());
-    return IL_OK;
+    return same_qr ? launch_cfg<NT, false, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                spins, diverged, energies, st)
+                   : launch_cfg<NT, false, false>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                 spins, diverged, energies, st);
 }
 
 // PCG64 advance-by-k constants: state_k = M^k state_0 + inc * (M^{k-1} + ... + 1)
@@ -346,7 +427,7 @@ bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       cudaStream_t st) {
+                       double* energies, cudaStream_t st) {
     if (!fast_anneal_supported(N, B, s)) {
         set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
         return IL_ERR_UNSUPPORTED;
@@ -366,13 +447,19 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.n_steps = s.n_steps;
     pcg_jump((2 * N + 2) / 2, &fs.jump_mult, &fs.jump_add);
     const bool split = precision != IL_PREC_TF32;
+    // x and e share their per-step factor exactly when zeta*dt == dt and
+    // 1 + dt (p - 1) == 1 + dt zeta a in FP32 (the reference defaults)
+    const bool same_qr = fs.alpha == fs.beta && fs.ndt == fs.ndtz;
+#define IL_NT(k) \
+    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, st)
     switch (N / 8) {
-        case 1: return launch_nt<1>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
-        case 2: return launch_nt<2>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
-        case 3: return launch_nt<3>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
-        case 4: return launch_nt<4>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
-        case 6: return launch_nt<6>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
-        case 8: return launch_nt<8>(G, g, b, base_seed, eps_p, P, B, fs, split, spins, diverged, st);
+        IL_NT(1);
+        IL_NT(2);
+        IL_NT(3);
+        IL_NT(4);
+        IL_NT(6);
+        IL_NT(8);
+#undef IL_NT
         default:
             set_error("fast anneal kernel not instantiated for n_dim=%d", N);
             return IL_ERR_UNSUPPORTED;

@@ -60,22 +60,28 @@ __device__ void gram_hermitian(const cplx* H, const cplx* y, int n_r, int n_t, c
 }
 
 // In-place lower Cholesky M = L L^H (M Hermitian positive definite, n <= 32,
-// lane i owns row i).  Returns false on a non-positive pivot (the reference
-// raises LinAlgError from cho_factor in that case).
-__device__ bool cholesky_lower(cplx* M, int n, int lane) {
+// lane i owns row i); inv_diag[k] = 1 / L[k][k] (scaling by the reciprocal,
+// as LAPACK's zpotrf does).  Returns false on a non-positive pivot (the
+// reference raises LinAlgError from cho_factor in that case).
+__device__ bool cholesky_lower(cplx* M, int n, double* inv_diag, int lane) {
     for (int k = 0; k < n; ++k) {
         const double piv = M[k * n + k].re;
         if (!(piv > 0.0)) return false;
         const double lkk = sqrt(piv);
+        const double inv = 1.0 / lkk;
         __syncwarp();
+        cplx lik = {0.0, 0.0};
         if (lane > k && lane < n) {
-            cplx v = M[lane * n + k];
-            M[lane * n + k] = {v.re / lkk, v.im / lkk};
+            const cplx v = M[lane * n + k];
+            lik = {v.re * inv, v.im * inv};
+            M[lane * n + k] = lik;
+        }
+        if (lane == k) {
+            M[k * n + k] = {lkk, 0.0};
+            inv_diag[k] = inv;
         }
         __syncwarp();
-        if (lane == k) M[k * n + k] = {lkk, 0.0};
         if (lane > k && lane < n) {
-            const cplx lik = M[lane * n + k];
             for (int j = k + 1; j <= lane; ++j) {
                 const cplx ljk = M[j * n + k];
                 // M[i][j] -= L[i][k] * conj(L[j][k])
@@ -89,23 +95,21 @@ __device__ bool cholesky_lower(cplx* M, int n, int lane) {
 }
 
 // Solve (L L^H) x = rhs in place (rhs -> x); L lower from cholesky_lower.
-__device__ void cholesky_solve(const cplx* L, int n, cplx* x, int lane) {
-    for (int k = 0; k < n; ++k) {  // L w = rhs
-        __syncwarp();
-        const double lkk = L[k * n + k].re;
-        const cplx wk = {x[k].re / lkk, x[k].im / lkk};
-        __syncwarp();
-        if (lane == k) x[k] = wk;
-        if (lane > k && lane < n) x[lane] = csub(x[lane], cmul(L[lane * n + k], wk));
+__device__ void cholesky_solve(const cplx* L, const double* inv_diag, int n, cplx* x, int lane) {
+    cplx xl = lane < n ? x[lane] : cplx{0.0, 0.0};
+    for (int k = 0; k < n; ++k) {  // L w = rhs (column sweep, rhs kept in registers)
+        const double inv = inv_diag[k];
+        const cplx xk = {__shfl_sync(kFull, xl.re, k) * inv, __shfl_sync(kFull, xl.im, k) * inv};
+        if (lane == k) xl = xk;
+        if (lane > k && lane < n) xl = csub(xl, cmul(L[lane * n + k], xk));
     }
     for (int k = n - 1; k >= 0; --k) {  // L^H x = w
-        __syncwarp();
-        const double lkk = L[k * n + k].re;
-        const cplx xk = {x[k].re / lkk, x[k].im / lkk};
-        __syncwarp();
-        if (lane == k) x[k] = xk;
-        if (lane < k) x[lane] = csub(x[lane], cmulc(L[k * n + lane], xk));
+        const double inv = inv_diag[k];
+        const cplx xk = {__shfl_sync(kFull, xl.re, k) * inv, __shfl_sync(kFull, xl.im, k) * inv};
+        if (lane == k) xl = xk;
+        if (lane < k) xl = csub(xl, cmulc(L[k * n + lane], xk));
     }
+    if (lane < n) x[lane] = xl;
     __syncwarp();
 }
 
@@ -171,47 +175,47 @@ __device__ double lambda_max_hermitian(cplx* A, int n, cplx* scratch, int lane) 
     __syncwarp();
     if (n == 1) return d[0];
 
-    // Gershgorin interval
-    double lo = DBL_MAX, hi = -DBL_MAX, emax2 = 0.0;
+    // Largest root of det(T - x I) by Laguerre iteration from the Gershgorin
+    // upper bound: for a polynomial with only real roots it converges
+    // monotonically from above to the largest root, cubically (and exactly
+    // in one step for a single multiple root).  Three-term recurrences give
+    // p, p', p'' without divisions; every lane iterates redundantly.
+    double hi = -DBL_MAX, lo = DBL_MAX;
     for (int i = 0; i < n; ++i) {
         const double r = (i > 0 ? e[i - 1] : 0.0) + (i < n - 1 ? e[i] : 0.0);
-        lo = fmin(lo, d[i] - r);
         hi = fmax(hi, d[i] + r);
-        if (i < n - 1) emax2 = fmax(emax2, e[i] * e[i]);
+        lo = fmin(lo, d[i] - r);
     }
-    const double pivmin = DBL_MIN * fmax(1.0, emax2);
-    const double span = fmax(hi - lo, DBL_MIN);
-    lo -= 2.0 * DBL_EPSILON * span;
-    hi += 2.0 * DBL_EPSILON * span;
-    for (int round = 0; round < 24; ++round) {
-        const double step = (hi - lo) / 33.0;
-        const double xl = lo + step * (double)(lane + 1);
-        // Sturm count of eigenvalues < xl
-        int cnt = 0;
-        double q = d[0] - xl;
-        if (fabs(q) < pivmin) q = -pivmin;
-        cnt += q < 0.0;
-        for (int i = 1; i < n; ++i) {
-            q = (d[i] - xl) - (e[i - 1] * e[i - 1]) / q;
-            if (fabs(q) < pivmin) q = -pivmin;
-            cnt += q < 0.0;
+    double x = hi + 4.0 * DBL_EPSILON * fmax(fabs(hi), fabs(hi - lo)) + DBL_MIN;
+    const double nn = (double)n;
+    for (int it = 0; it < 64; ++it) {
+        double p0 = 1.0, p1 = 0.0, p2 = 0.0;      // P_{k-1}, P'_{k-1}, P''_{k-1}
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0;      // P_{k-2}, ...
+        for (int k = 0; k < n; ++k) {
+            const double dk = d[k] - x;
+            const double e2 = k > 0 ? e[k - 1] * e[k - 1] : 0.0;
+            const double r0 = dk * p0 - e2 * q0;
+            const double r1 = dk * p1 - e2 * q1 - p0;
+            const double r2 = dk * p2 - e2 * q2 - 2.0 * p1;
+            q0 = p0; q1 = p1; q2 = p2;
+            p0 = r0; p1 = r1; p2 = r2;
+            const double mag = fabs(p0);
+            if (mag > 1e150 || (mag < 1e-150 && mag > 0.0)) {
+                const double sc = mag > 1e150 ? 1e-150 : 1e150;
+                p0 *= sc; p1 *= sc; p2 *= sc; q0 *= sc; q1 *= sc; q2 *= sc;
+            }
         }
-        const unsigned above = __ballot_sync(kFull, cnt == n);
-        double nlo, nhi;
-        if (above == 0u) {
-            nlo = __shfl_sync(kFull, xl, 31);
-            nhi = hi;
-        } else {
-            const int l = __ffs(above) - 1;
-            nhi = __shfl_sync(kFull, xl, l);
-            nlo = l > 0 ? __shfl_sync(kFull, xl, l - 1) : lo;
-        }
-        const bool stalled = (nlo == lo && nhi == hi);
-        lo = nlo;
-        hi = nhi;
-        if (stalled || hi - lo <= 4.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) break;
+        if (p0 == 0.0) break;  // landed on the root
+        const double G = p1 / p0;
+        const double Hh = G * G - p2 / p0;
+        const double disc = fmax((nn - 1.0) * (nn * Hh - G * G), 0.0);
+        const double den = G + sqrt(disc);
+        if (!(den > 0.0)) break;
+        const double step = nn / den;
+        x -= step;
+        if (!(step > 2.0 * DBL_EPSILON * fabs(x))) break;
     }
-    return 0.5 * (lo + hi);
+    return x;
 }
 
 // Per-warp shared-memory carve-up for the detection front-end.
@@ -335,10 +339,11 @@ __global__ void k_front(const double* __restrict__ Hg, const double* __restrict_
             sm.M[i] = a;
         }
         __syncwarp();
-        const bool ok = cholesky_lower(sm.M, n_t, lane);
+        double* invd = reinterpret_cast<double*>(sm.scr);
+        const bool ok = cholesky_lower(sm.M, n_t, invd, lane);
         if (status && lane == 0) status[prob] = ok ? 0 : -1;
         if (ok) {
-            cholesky_solve(sm.M, n_t, sm.z, lane);
+            cholesky_solve(sm.M, invd, n_t, sm.z, lane);
             for (int j = lane; j < n_t; j += 32) {
                 idx[2 * j] = (uint8_t)level_index(sm.z[j].re, al);
                 idx[2 * j + 1] = (uint8_t)level_index(sm.z[j].im, al);
@@ -367,7 +372,8 @@ int front_blocks(int64_t P, size_t per_warp, int* wpb, size_t* smem) {
 __global__ void k_select_decode(const double* __restrict__ Hg, const double* __restrict__ yg,
                                 const double* __restrict__ Gg, const double* __restrict__ bg,
                                 const double* __restrict__ offset, const int8_t* __restrict__ spins,
-                                const uint8_t* __restrict__ diverged, int64_t P, int n_r, int n_t,
+                                const uint8_t* __restrict__ diverged,
+                                const double* __restrict__ energies, int64_t P, int n_r, int n_t,
                                 int B, Alphabet al, uint8_t* __restrict__ x_idx,
                                 double* __restrict__ energy, int8_t* __restrict__ source,
                                 int32_t* __restrict__ anneal_index,
@@ -406,7 +412,9 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
         if (a < B) {
             const bool dv = diverged[prob * B + a] != 0;
             ndiv += dv;
-            if (!dv) {
+            if (!dv && energies) {
+                ea = energies[prob * B + a];
+            } else if (!dv) {
                 const int8_t* s = sp0 + (int64_t)a * S;
                 double quad = 0.0, lin = 0.0;
                 for (int i = 0; i < N; ++i) {
@@ -517,7 +525,9 @@ __global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __re
         L[j * n_u + i] = {re, -im};
     }
     __syncwarp();
-    const bool ok = cholesky_lower(L, n_u, lane);
+    __shared__ double invd_all[8][32];
+    double* invd = invd_all[warp];
+    const bool ok = cholesky_lower(L, n_u, invd, lane);
     if (lane == 0 && status) status[prob] = ok ? 0 : -1;
     // X = A^-1 H, one column per lane
     for (int col = lane; col < n_ant; col += 32) {
@@ -623,7 +633,7 @@ __global__ void k_add_i32(const int32_t* __restrict__ a, int64_t n, int32_t* __r
 
 int launch_add_i32(const int32_t* a, int64_t n, int32_t* acc, cudaStream_t st) {
     if (n == 0) return IL_OK;
-    k_add_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, n, acc);
+    IL_LAUNCH(kProfOther, st, k_add_i32<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, n, acc););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -647,8 +657,8 @@ int launch_mmse(const double* H, const double* y, const double* noise_var, int64
     int rc = set_smem((const void*)k_front<true, false>, smem);
     if (rc) return rc;
     IsingOut o{};
-    k_front<true, false><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
-                                                          energy, status, o);
+    IL_LAUNCH(kProfFront, st, k_front<true, false><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
+                                                          energy, status, o););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -664,9 +674,9 @@ int launch_build_ising(const double* H, const double* y, const uint8_t* guess_id
     int rc = set_smem((const void*)k_front<false, true>, smem);
     if (rc) return rc;
     IsingOut o{G, g_diag, b, offset, eps_scale, eps_out, eps_gain, fixed_eps};
-    k_front<false, true><<<blocks, 32 * wpb, smem, st>>>(H, y, nullptr, P, n_r, n_t, al,
+    IL_LAUNCH(kProfFront, st, k_front<false, true><<<blocks, 32 * wpb, smem, st>>>(H, y, nullptr, P, n_r, n_t, al,
                                                           const_cast<uint8_t*>(guess_idx),
-                                                          nullptr, nullptr, o);
+                                                          nullptr, nullptr, o););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -682,17 +692,18 @@ int launch_mmse_ising(const double* H, const double* y, const double* noise_var,
     int rc = set_smem((const void*)k_front<true, true>, smem);
     if (rc) return rc;
     IsingOut o{G, g_diag, b, offset, nullptr, eps_out, eps_gain, fixed_eps};
-    k_front<true, true><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
-                                                         energy, status, o);
+    IL_LAUNCH(kProfFront, st, k_front<true, true><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
+                                                         energy, status, o););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
 
 int launch_select_decode(const double* H, const double* y, const double* G, const double* b,
                          const double* offset, const int8_t* spins, const uint8_t* diverged,
-                         int64_t P, int n_r, int n_t, int B, const Alphabet& al,
-                         uint8_t* x_idx_io, double* energy_io, int8_t* source,
-                         int32_t* anneal_index, int32_t* diverged_count, cudaStream_t st) {
+                         const double* energies, int64_t P, int n_r, int n_t, int B,
+                         const Alphabet& al, uint8_t* x_idx_io, double* energy_io,
+                         int8_t* source, int32_t* anneal_index, int32_t* diverged_count,
+                         cudaStream_t st) {
     if (P == 0) return IL_OK;
     const int N = 2 * n_t;
     IL_REQUIRE(2 * n_t <= 128, "n_t too large");
@@ -704,9 +715,9 @@ int launch_select_decode(const double* H, const double* y, const double* G, cons
     int rc = set_smem((const void*)k_select_decode, smem);
     if (rc) return rc;
     const int blocks = (int)((P + wpb - 1) / wpb);
-    k_select_decode<<<blocks, 32 * wpb, smem, st>>>(H, y, G, b, offset, spins, diverged, P, n_r,
+    IL_LAUNCH(kProfSelect, st, k_select_decode<<<blocks, 32 * wpb, smem, st>>>(H, y, G, b, offset, spins, diverged, energies, P, n_r,
                                                     n_t, B, al, x_idx_io, energy_io, source,
-                                                    anneal_index, diverged_count);
+                                                    anneal_index, diverged_count););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -722,8 +733,8 @@ int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, in
     int rc = set_smem((const void*)k_zf_vpp_front, smem);
     if (rc) return rc;
     const int blocks = (int)((P + wpb - 1) / wpb);
-    k_zf_vpp_front<<<blocks, 32 * wpb, smem, st>>>(H, u, P, n_u, n_ant, tau, W, y_t, H_p,
-                                                   base_energy, status);
+    IL_LAUNCH(kProfFront, st, k_zf_vpp_front<<<blocks, 32 * wpb, smem, st>>>(H, u, P, n_u, n_ant, tau, W, y_t, H_p,
+                                                   base_energy, status););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -735,8 +746,8 @@ int launch_vpp_post(const double* W, const double* u, const double* y_t, const d
     IL_REQUIRE(n_ant <= 64, "n_ant > 64 not supported");
     const int wpb = 4;
     const int blocks = (int)((P + wpb - 1) / wpb);
-    k_vpp_post<<<blocks, 32 * wpb, 0, st>>>(W, u, y_t, base_energy, vidx, P, n_u, n_ant, reach,
-                                            tau, sqrt(power), x, v, unnorm_power);
+    IL_LAUNCH(kProfOther, st, k_vpp_post<<<blocks, 32 * wpb, 0, st>>>(W, u, y_t, base_energy, vidx, P, n_u, n_ant, reach,
+                                            tau, sqrt(power), x, v, unnorm_power););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -744,7 +755,7 @@ int launch_vpp_post(const double* W, const double* u, const double* y_t, const d
 int launch_base_seeds(const uint64_t* seed, int64_t P, uint64_t k1, uint64_t k2,
                       uint64_t* base_out, cudaStream_t st) {
     if (P == 0) return IL_OK;
-    k_base_seeds<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(seed, P, k1, k2, base_out);
+    IL_LAUNCH(kProfOther, st, k_base_seeds<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(seed, P, k1, k2, base_out););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -771,7 +782,7 @@ int launch_gray_demap(const uint8_t* x_idx, int64_t n_sym, int bits_per_dim, uin
     IL_REQUIRE(bits_per_dim >= 1 && bits_per_dim <= 8, "bits_per_dim must be in [1, 8]");
     const int64_t n = 2 * n_sym;
     if (n == 0) return IL_OK;
-    k_gray_demap<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x_idx, n, bits_per_dim, bits);
+    IL_LAUNCH(kProfOther, st, k_gray_demap<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x_idx, n, bits_per_dim, bits););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }

@@ -27,7 +27,7 @@ int launch_anneal_exact(const double* G, const double* g, const double* b, const
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       cudaStream_t st);
+                       double* energies, cudaStream_t st);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
 
 // ---- front-end / reduction kernels -----------------------------------------
@@ -54,7 +54,8 @@ int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, in
 // x_idx_io holds the guess on entry and the result on exit.
 int launch_select_decode(const double* H, const double* y, const double* G, const double* b,
                          const double* offset, const int8_t* spins, const uint8_t* diverged,
-                         int64_t P, int n_r, int n_t, int B, const Alphabet& al,
+                         const double* energies, int64_t P, int n_r, int n_t, int B,
+                         const Alphabet& al,
                          uint8_t* x_idx_io, double* energy_io, int8_t* source,
                          int32_t* anneal_index, int32_t* diverged_count, cudaStream_t st);
 
@@ -72,12 +73,24 @@ int launch_gray_demap(const uint8_t* x_idx, int64_t n_sym, int bits_per_dim, uin
 int launch_base_seeds(const uint64_t* seed, int64_t P, uint64_t k1, uint64_t k2,
                       uint64_t* base_out, cudaStream_t st);
 
+// ---- measurement hooks (prof.cu) -------------------------------------------
+enum ProfKind { kProfFront = 0, kProfAnneal = 1, kProfSelect = 2, kProfOther = 3 };
+int prof_start(int kind, cudaStream_t st);  // counts the launch; events only when profiling
+void prof_stop(int idx, cudaStream_t st);
+
+#define IL_LAUNCH(kind, st, ...)                          \
+    do {                                                  \
+        const int _pi = ::il::prof_start((kind), (st));   \
+        __VA_ARGS__;                                      \
+        ::il::prof_stop(_pi, (st));                       \
+    } while (0)
+
 // ---- workspace (stream-ordered pool allocations) ----------------------------
 struct Workspace {
     cudaStream_t st;
     void* ptrs[32];
     int n = 0;
-    explicit Workspace(cudaStream_t s) : st(s) {}
+    explicit Workspace(cudaStream_t s);
     ~Workspace();
     template <class T>
     T* get(size_t count, int* rc) {

@@ -34,8 +34,9 @@ int il_derive_seeds(const uint64_t* parts, int32_t n_parts, int64_t n, uint64_t*
     IL_REQUIRE(n_parts >= 1 && n_parts <= 6, "n_parts must be in [1, 6]");
     IL_REQUIRE(n >= 0, "negative count");
     if (n == 0) return IL_OK;
-    il::k_derive_seeds<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(parts, n_parts,
-                                                                                    n, out);
+    cudaStream_t st = (cudaStream_t)stream;
+    IL_LAUNCH(il::kProfOther, st,
+              il::k_derive_seeds<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(parts, n_parts, n, out));
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -46,8 +47,10 @@ int il_initial_states(const uint64_t* seeds, int64_t n, int32_t S, double amplit
     IL_REQUIRE(amplitude > 0, "init_amplitude must be positive");
     if (n == 0 || S == 0) return IL_OK;
     const double lo = -amplitude, range = amplitude - lo;
-    il::k_initial_states<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
-        seeds, n, S, lo, range, x0);
+    cudaStream_t st = (cudaStream_t)stream;
+    IL_LAUNCH(il::kProfOther, st,
+              il::k_initial_states<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(seeds, n, S, lo,
+                                                                                 range, x0));
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }

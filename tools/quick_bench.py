@@ -25,6 +25,9 @@ def run(n_t, order, P, prec, reps=3):
     ms = min(ts)
     print(f"n_t={n_t} M={order} P={P} {prec}: {ms:.3f} ms  {P / ms * 1e3 / 1e6:.3f} Mdet/s", flush=True)
 
-for prec in ("fp32", "tf32", "fp64_exact"):
-    run(16, 16, 45864 if prec != "fp64_exact" else 4096, prec)
-    run(8, 16, 45864 if prec != "fp64_exact" else 4096, prec)
+if len(sys.argv) > 1:
+    run(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], int(sys.argv[5]) if len(sys.argv) > 5 else 3)
+else:
+    for prec in ("fp32", "tf32", "fp64_exact"):
+        run(16, 16, 45864 if prec != "fp64_exact" else 4096, prec)
+        run(8, 16, 45864 if prec != "fp64_exact" else 4096, prec)
