@@ -117,6 +117,29 @@ int il_build_ising_batch(const double* H, const double* y, const uint8_t* guess_
                          double* eps_scale, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Solver on given Ising problems (solver.py:217-279).
+ *   il_spin_energies — E(s) = u'Gu - 2 tr G + 2 s_aux b'u, u = s_A + s_B
+ *     (solver.py:171-175, transform.py:143-152) for spins[P*n_batch*(2N+1)].
+ *   il_solve_batch — P x solve_batch: anneal r of problem p starts from
+ *     default_rng(derive_seed(base_seed[p], r)).uniform(-amp, amp); returns
+ *     the best non-diverged anneal (strict <, lowest index on ties) in
+ *     best_spins[P*(2N+1)], best_energy[P], best_index[P] (-1 when every
+ *     anneal diverged or best_energy + offset > fallback_energy, i.e. when
+ *     the reference returns None), diverged_count[P].  eps[P] is the
+ *     resolved coupling.  steps/mvms [P*n_anneals] (optional) request the
+ *     FP64-exact kernel, whose halting step is part of its contract.
+ * ------------------------------------------------------------------------- */
+int il_spin_energies(const double* G, const double* g_diag, const double* b,
+                     const int8_t* spins, int64_t P, int32_t n_batch, int32_t n_dim,
+                     double* energies, void* stream);
+int il_solve_batch(const double* G, const double* g_diag, const double* b,
+                   const double* offset, const double* fallback_energy, const double* eps,
+                   const uint64_t* base_seed, int64_t P, int32_t n_dim,
+                   const il_cac_params* prm, int8_t* best_spins, double* best_energy,
+                   int32_t* best_index, int32_t* diverged_count, int64_t* steps,
+                   int64_t* mvms, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Batched uplink detection: P x detect_cim (detector.py:57-82) with
  * seed[p] the `seed` argument of detect_cim for problem p.  Outputs:
  *   x_idx[P*n_t*2] level indices (re, im) of x_hard,

@@ -11,7 +11,9 @@ import ctypes
 import os
 import threading
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libisinglink_b200.so")
+LIB_PATH = os.environ.get(
+    "ISINGLINK_B200_LIB",
+    os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libisinglink_b200.so"))
 
 IL_OK, IL_ERR_ARG, IL_ERR_CUDA, IL_ERR_UNSUPPORTED, IL_ERR_NOMEM = 0, -1, -2, -3, -4
 PREC = {"fp64_exact": 0, "fp32": 1, "tf32": 2}
@@ -51,6 +53,10 @@ _SIGS = {
                               ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp],
                              ctypes.c_int),
     "il_gray_demap": ([_vp, _c_i64, _c_i32, _vp, _vp], ctypes.c_int),
+    "il_spin_energies": ([_vp, _vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _vp, _vp], ctypes.c_int),
+    "il_solve_batch": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32,
+                        ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                       ctypes.c_int),
     "il_kernel_launches": ([], ctypes.c_longlong),
     "il_profile_begin": ([], None),
     "il_profile_end": ([_vp, _vp, ctypes.c_int], ctypes.c_int),

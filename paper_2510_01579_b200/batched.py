@@ -209,3 +209,56 @@ def gray_demap(x_idx, bits_per_dim: int) -> torch.Tensor:
     out = torch.empty(xd.shape[:-1] + (2 * bits_per_dim,), dtype=torch.uint8, device=xd.device)
     _lib.call("il_gray_demap", xd.data_ptr(), n_sym, int(bits_per_dim), out.data_ptr(), _stream())
     return out
+
+
+def spin_energies(G, b, spins) -> torch.Tensor:
+    """E(s) per spin row (solver.py:171-175).  G [P,N,N], b [P,N], spins [P,B,2N+1]."""
+    Gd = _dev(G, torch.float64)
+    bd = _dev(b, torch.float64)
+    sd = _dev(spins, torch.int8)
+    P, N = bd.shape
+    B = sd.shape[1]
+    out = torch.empty((P, B), dtype=torch.float64, device=Gd.device)
+    _lib.call("il_spin_energies", Gd.data_ptr(), 0, bd.data_ptr(), sd.data_ptr(), P, B, N,
+              out.data_ptr(), _stream())
+    return out
+
+
+@dataclass
+class SolveBatch:
+    best_spins: torch.Tensor     # int8 [P, 2N+1]
+    best_energy: torch.Tensor    # f64 [P] Ising energy of the best survivor (inf if none)
+    best_index: torch.Tensor     # int32 [P]; -1 where the reference returns None
+    diverged: torch.Tensor       # int32 [P]
+    steps: torch.Tensor | None = None  # int64 [P, B] (FP64-exact only)
+    mvms: torch.Tensor | None = None
+
+
+def solve_batch(G, g_diag, b, offset, fallback_energy, eps, base_seeds, params=None,
+                precision: str | None = None, counts: bool = False) -> SolveBatch:
+    """P x ``solve_batch`` (solver.py:238-279) on given Ising problems."""
+    params = params or CacParams()
+    prm = to_c(params, precision)
+    Gd = _dev(G, torch.float64)
+    P, N, _ = Gd.shape
+    gd = _dev(g_diag, torch.float64)
+    bd = _dev(b, torch.float64)
+    od = _dev(offset, torch.float64).reshape(P)
+    fd = _dev(fallback_energy, torch.float64).reshape(P)
+    ed = _dev(eps, torch.float64).reshape(P)
+    sd = _seeds(base_seeds, P)
+    dev = Gd.device
+    B = int(params.n_anneals)
+    out = SolveBatch(best_spins=torch.empty((P, 2 * N + 1), dtype=torch.int8, device=dev),
+                     best_energy=torch.empty(P, dtype=torch.float64, device=dev),
+                     best_index=torch.empty(P, dtype=torch.int32, device=dev),
+                     diverged=torch.empty(P, dtype=torch.int32, device=dev))
+    if counts:
+        out.steps = torch.empty((P, B), dtype=torch.int64, device=dev)
+        out.mvms = torch.empty((P, B), dtype=torch.int64, device=dev)
+    _lib.call("il_solve_batch", Gd.data_ptr(), gd.data_ptr(), bd.data_ptr(), od.data_ptr(),
+              fd.data_ptr(), ed.data_ptr(), sd.data_ptr(), P, N, prm,
+              out.best_spins.data_ptr(), out.best_energy.data_ptr(), out.best_index.data_ptr(),
+              out.diverged.data_ptr(), out.steps.data_ptr() if counts else None,
+              out.mvms.data_ptr() if counts else None, _stream())
+    return out

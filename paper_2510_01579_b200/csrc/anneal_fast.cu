@@ -33,6 +33,8 @@
 //
 // Scaling: G, g, b are pre-multiplied by -dt*eps so that the MMA directly
 // yields the -dt*eps*c term of the update.
+#include <cuda_fp16.h>
+
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
 
@@ -41,6 +43,12 @@ namespace il {
 namespace {
 
 constexpr int kWarpsPerCta = 4;
+#ifndef IL_SPLIT_ACC
+#define IL_SPLIT_ACC 0
+#endif
+#ifndef IL_FAST_MINB
+#define IL_FAST_MINB 3
+#endif
 
 struct FastScalars {
     float alpha;    // 1 + dt (p - 1)
@@ -55,16 +63,21 @@ struct FastScalars {
     int f_mvm, n_steps;
 };
 
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// hi + lo split of a float pair into two packed f16x2 words (x in the low half)
+__device__ __forceinline__ void split_h2(float2 v, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __float22half2_rn(v);
+    const float2 hf = __half22float2(h);
+    const float2 r = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
+    hi = h2_bits(h);
+    lo = h2_bits(__float22half2_rn(r));
 }
 
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
-                                         uint32_t b1) {
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
+                                        uint32_t b1) {
     asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
         "{%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
@@ -88,7 +101,7 @@ __device__ __forceinline__ float max_nan(float a, float b) {
 // x2 of the incoming state is folded into the divergence max.
 template <bool SAME_QR>
 __device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
-                                           const FastScalars& s, float& dv) {
+                                           const FastScalars& s, float e_floor, float& dv) {
     const float2 x2 = __fmul2_rn(x, x);
     dv = max_nan3(dv, x2.x, x2.y);
     const float2 q = __ffma2_rn(make_float2(s.ndt, s.ndt), x2, make_float2(s.alpha, s.alpha));
@@ -99,32 +112,41 @@ __device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
     const float2 t = __fmul2_rn(x, q);
     x = __ffma2_rn(e, C, t);
     const float2 er = __fmul2_rn(e, r);
-    e = make_float2(fmaxf(er.x, s.e_floor), fmaxf(er.y, s.e_floor));
+    e = make_float2(fmaxf(er.x, e_floor), fmaxf(er.y, e_floor));
 }
 
 template <bool SAME_QR>
 __device__ __forceinline__ void euler_one(float& x, float& e, const float C, const FastScalars& s,
-                                          float& dv) {
+                                          float e_floor, float& dv) {
     const float x2 = x * x;
     dv = max_nan(dv, x2);
     const float q = fmaf(s.ndt, x2, s.alpha);
     const float r = SAME_QR ? q : fmaf(s.ndtz, x2, s.beta);
     x = fmaf(e, C, x * q);
-    e = fmaxf(e * r, s.e_floor);
+    e = fmaxf(e * r, e_floor);
 }
 
 template <int NT>
 struct FastLayout {
     static constexpr int N = 8 * NT;
     static constexpr int S = 2 * N + 1;
-    static constexpr int kFragF4 = NT * NT * 32;          // float4 per warp
+    static constexpr int KT = (NT + 1) / 2;               // k16 tiles of the f16 MMA
+    static constexpr int kFragF4 = KT * NT * 32;          // uint4 per warp
     static constexpr int kX0F4 = (16 * S + 3) / 4;        // x0 staging, aliased
     static constexpr int kWarpF4 = kFragF4 > kX0F4 ? kFragF4 : kX0F4;
     static constexpr size_t kSmem = sizeof(float4) * kWarpsPerCta * kWarpF4;
 };
 
+// Tensor-core operand scaling.  The coupling product runs on f16 operands
+// (11-bit significand, like TF32, at twice the K per instruction).  To keep
+// the lo parts of the split out of the f16 subnormal range, -K*G is scaled
+// by 2^sc per problem so that its largest entry lies in [128, 256).  The
+// scale is carried, exactly, by the error variables: every coupling term
+// enters the update as e*C, so storing e_s = e * 2^-sc and C_s = C * 2^sc
+// leaves e*C unchanged, and e' = max(floor, e r) becomes
+// e_s' = max(floor * 2^-sc, e_s r) -- power-of-two scalings are exact.
 template <int NT, bool SPLIT, bool SAME_QR>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 3)
+__global__ void __launch_bounds__(kWarpsPerCta * 32, NT <= 2 ? 4 : (NT <= 4 ? IL_FAST_MINB : 1))
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
               const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
@@ -133,19 +155,19 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     using L = FastLayout<NT>;
     constexpr int N = L::N;
     constexpr int S = L::S;
-    extern __shared__ __align__(16) float4 smem_f4[];
+    constexpr int KT = L::KT;
+    extern __shared__ __align__(16) uint4 smem_u4[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerCta + warp;
     if (task >= n_tasks) return;
     const int64_t prob = task / tiles_per_prob;
     const int mt = (int)(task % tiles_per_prob);
     const int B = tiles_per_prob * 16;
-    float4* frag = smem_f4 + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
+    uint4* frag = smem_u4 + warp * L::kWarpF4;       // G fragments (after x0 is consumed)
     float* x0s = reinterpret_cast<float*>(frag);      // x0 staging [16][S]
 
     const int g = lane >> 2, t = lane & 3;
     const int hown = t & 1;  // the aux spin of anneal g + 8*hown is integrated by this lane
-    const double K = s.dt * eps_p[prob];
     const double* G = Gall + prob * (int64_t)N * N;
 
     // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
@@ -159,6 +181,20 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         const int i0 = part ? S0 : 0, i1 = part ? S : S0;
         for (int i = i0; i < i1; ++i) x0s[al * S + i] = (float)rng.uniform(s.x0_lo, s.x0_range);
     }
+
+    // ---- per-problem scale 2^sc for -K*G ------------------------------------
+    const double K = s.dt * eps_p[prob];
+    double gmax = 0.0;
+    for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(__ldg(G + i)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+    int ex = 0;
+    frexp(K * gmax, &ex);
+    const int sc = (K * gmax > 0.0) ? 8 - ex : 0;
+    const double Ks = ldexp(K, sc);
+    const float e_init = ldexpf(1.0f, -sc);
+    const float e_floor = ldexpf(s.e_floor, -sc);
+
     __syncwarp();
     float2 xA[2][NT], xB[2][NT], eA[2][NT], eB[2][NT], CA[2][NT], CB[2][NT];
 #pragma unroll
@@ -169,35 +205,40 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             const int i = 8 * n + 2 * t;
             xA[h][n] = make_float2(r[i], r[i + 1]);
             xB[h][n] = make_float2(r[N + i], r[N + i + 1]);
-            eA[h][n] = eB[h][n] = make_float2(1.f, 1.f);
+            eA[h][n] = eB[h][n] = make_float2(e_init, e_init);
             CA[h][n] = CB[h][n] = make_float2(0.f, 0.f);
         }
     }
-    float xa = x0s[(g + 8 * hown) * S + 2 * N], ea = 1.f, Ca = 0.f, dva = 0.f;
-    float dv[2] = {0.f, 0.f};
+    float xa = x0s[(g + 8 * hown) * S + 2 * N], ea = e_init, Ca = 0.f, dva = 0.f;
+    float dv[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
     __syncwarp();
 
-    // ---- stage -K*G as permuted TF32 B fragments (hi, lo) ------------------
+    // ---- stage -Ks*G as f16 B fragments (hi, lo) of m16n8k16 --------------
+    // b0 = B[16kt+2t, +1][8n+g], b1 = B[16kt+8+2t, +1][8n+g]; rows >= N are zero
 #pragma unroll
-    for (int kt = 0; kt < NT; ++kt) {
+    for (int kt = 0; kt < KT; ++kt) {
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-            const float f0 = (float)(-K * __ldg(G + (8 * kt + 2 * t) * N + 8 * n + g));
-            const float f1 = (float)(-K * __ldg(G + (8 * kt + 2 * t + 1) * N + 8 * n + g));
-            const uint32_t h0 = to_tf32(f0), h1 = to_tf32(f1);
-            const uint32_t l0 = to_tf32(f0 - __uint_as_float(h0));
-            const uint32_t l1 = to_tf32(f1 - __uint_as_float(h1));
-            frag[(kt * NT + n) * 32 + lane] = make_float4(__uint_as_float(h0), __uint_as_float(h1),
-                                                          __uint_as_float(l0), __uint_as_float(l1));
+            const int c = 8 * n + g;
+            float f[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = 16 * kt + 2 * t + (q & 1) + 8 * (q >> 1);
+                f[q] = r < N ? (float)(-Ks * __ldg(G + r * N + c)) : 0.f;
+            }
+            uint32_t h01, l01, h23, l23;
+            split_h2(make_float2(f[0], f[1]), h01, l01);
+            split_h2(make_float2(f[2], f[3]), h23, l23);
+            frag[(kt * NT + n) * 32 + lane] = make_uint4(h01, h23, l01, l23);
         }
     }
-    // per-thread spin constants: K g_i and -K b_i for spins 8n+2t+{0,1}
+    // per-thread spin constants: Ks g_i and -Ks b_i for spins 8n+2t+{0,1}
     float2 Kg[NT], nKb[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
         const int i = 8 * n + 2 * t;
-        Kg[n] = make_float2((float)(K * gall[prob * N + i]), (float)(K * gall[prob * N + i + 1]));
-        nKb[n] = make_float2((float)(-K * ball[prob * N + i]), (float)(-K * ball[prob * N + i + 1]));
+        Kg[n] = make_float2((float)(Ks * gall[prob * N + i]), (float)(Ks * gall[prob * N + i + 1]));
+        nKb[n] = make_float2((float)(-Ks * ball[prob * N + i]), (float)(-Ks * ball[prob * N + i + 1]));
     }
     __syncwarp();
 
@@ -205,7 +246,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     for (int step = 0; step < s.n_steps; ++step) {
         if (until_refresh == 0) {
             until_refresh = s.f_mvm;
-            // ---- refresh: v = x1 + x2, M' = -K G v on tensor cores ------------
+            // ---- refresh: v = x1 + x2, M' = -Ks G v on tensor cores -----------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
 #pragma unroll
@@ -222,7 +263,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             {
                 const float mine = hown ? pb[1] : pb[0];
                 const float other = hown ? pb[0] : pb[1];
-                // quad sum of the own anneal's partials: lanes t and t^2 share hown
+                // quad sum of the own anneal's partials; the two owner lanes of an
+                // anneal (t, t^2) add the same four terms in commuted order, so
+                // their aux trajectories stay bit-identical
                 float tot = mine + __shfl_xor_sync(0xffffffffu, other, 1);
                 tot += __shfl_xor_sync(0xffffffffu, tot, 2);
                 Ca = tot;
@@ -230,34 +273,51 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             float acc[NT][4];
 #pragma unroll
             for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+#if IL_SPLIT_ACC
+            float acc2[NT][4];
 #pragma unroll
-            for (int kt = 0; kt < NT; ++kt) {
-                const float av[4] = {v[0][kt].x, v[1][kt].x, v[0][kt].y, v[1][kt].y};
+            for (int n = 0; n < NT; ++n) acc2[n][0] = acc2[n][1] = acc2[n][2] = acc2[n][3] = 0.f;
+#endif
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                // A fragment: a0 = (g, 2t..), a1 = (g+8, 2t..), a2 = (g, 2t+8..), a3 = (g+8, 2t+8..)
                 uint32_t ahi[4], alo[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    ahi[q] = to_tf32(av[q]);
-                    // hardware ignores the low 13 bits of a TF32 operand: the lo
-                    // part is passed unrounded (truncated), error ~2^-21 relative
-                    alo[q] = __float_as_uint(av[q] - __uint_as_float(ahi[q]));
+                split_h2(v[0][2 * kt], ahi[0], alo[0]);
+                split_h2(v[1][2 * kt], ahi[1], alo[1]);
+                if (2 * kt + 1 < NT) {
+                    split_h2(v[0][2 * kt + 1], ahi[2], alo[2]);
+                    split_h2(v[1][2 * kt + 1], ahi[3], alo[3]);
+                } else {
+                    ahi[2] = ahi[3] = alo[2] = alo[3] = 0u;
                 }
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
-                    const float4 f = frag[(kt * NT + n) * 32 + lane];
+                    const uint4 f = frag[(kt * NT + n) * 32 + lane];
                     if (SPLIT) {
-                        mma_tf32(acc[n], alo, __float_as_uint(f.x), __float_as_uint(f.y));
-                        mma_tf32(acc[n], ahi, __float_as_uint(f.z), __float_as_uint(f.w));
+#if IL_SPLIT_ACC
+                        mma_f16(acc2[n], alo, f.x, f.y);
+                        mma_f16(acc2[n], ahi, f.z, f.w);
+#else
+                        mma_f16(acc[n], alo, f.x, f.y);
+                        mma_f16(acc[n], ahi, f.z, f.w);
+#endif
                     }
-                    mma_tf32(acc[n], ahi, __float_as_uint(f.x), __float_as_uint(f.y));
+                    mma_f16(acc[n], ahi, f.x, f.y);
                 }
             }
-            // ---- coupling assembly: C = M' + K g x_self - K b xa -------------
+            // ---- coupling assembly: C_s = M' + Ks g x_self - Ks b xa ----------
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const float xah = h ? xa1 : xa0;
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
+#if IL_SPLIT_ACC
+                    const float2 m2 = SPLIT ? __fadd2_rn(make_float2(acc2[n][2 * h], acc2[n][2 * h + 1]),
+                                                         make_float2(acc[n][2 * h], acc[n][2 * h + 1]))
+                                            : make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
+#else
                     const float2 m2 = make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
+#endif
                     const float2 u2 = __ffma2_rn(nKb[n], make_float2(xah, xah), m2);
                     CA[h][n] = __ffma2_rn(Kg[n], xA[h][n], u2);
                     CB[h][n] = __ffma2_rn(Kg[n], xB[h][n], u2);
@@ -268,11 +328,11 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-                euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, dv[h]);
-                euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, dv[h]);
+                euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, e_floor, dv[h][n & 1]);
+                euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
             }
         }
-        euler_one<SAME_QR>(xa, ea, Ca, s, dva);
+        euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
         --until_refresh;
     }
 
@@ -280,15 +340,13 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     // E = u'Gu - 2 tr G + 2 s_aux b'u with u = s_A + s_B (solver.py:171-175)
     const float xa_h[2] = {__shfl_sync(0xffffffffu, xa, (lane & ~3) | 0),
                            __shfl_sync(0xffffffffu, xa, (lane & ~3) | 1)};
-    {
-        float d = max_nan(dva, xa * xa);  // own aux: fold into dv of its anneal
-        dv[hown] = max_nan(dv[hown], d);
-    }
+    float dvh[2] = {max_nan(dv[0][0], dv[0][1]), max_nan(dv[1][0], dv[1][1])};
+    dvh[hown] = max_nan(dvh[hown], max_nan(dva, xa * xa));  // own aux spin
     const int64_t row0 = prob * (int64_t)B + mt * 16;
     uint64_t pos[2], neg[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        float d = dv[h];
+        float d = dvh[h];
         uint64_t pm = 0, nm = 0;
         const int64_t row = row0 + g + 8 * h;
         int8_t* sp = spins + row * S;
@@ -317,35 +375,40 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         if (t == h) sp[2 * N] = xa >= 0.f ? 1 : -1;
         if (t == 0) diverged[row] = (d <= s.thr2) ? 0 : 1;
     }
-    // partial quadratic / linear / trace terms over this lane's rows
+    // FP64 energies.  Row sums use G's symmetry: sum_j s_j G[j][i] reads row j
+    // at this lane's columns i = 8n+2t+{0,1} (16-byte loads), with s_j decoded
+    // once per j for both anneals.
     const double* bg = ball + prob * N;
+    double rs[2][2 * NT];
+#pragma unroll
+    for (int k = 0; k < 2 * NT; ++k) rs[0][k] = rs[1][k] = 0.0;
+    for (int j = 0; j < N; ++j) {
+        const double s0 = (double)((int)((pos[0] >> j) & 1u) - (int)((neg[0] >> j) & 1u));
+        const double s1 = (double)((int)((pos[1] >> j) & 1u) - (int)((neg[1] >> j) & 1u));
+        const double* Gj = G + (int64_t)j * N + 2 * t;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+            const double2 gv = __ldg(reinterpret_cast<const double2*>(Gj + 8 * n));
+            rs[0][2 * n] = fma(gv.x, s0, rs[0][2 * n]);
+            rs[0][2 * n + 1] = fma(gv.y, s0, rs[0][2 * n + 1]);
+            rs[1][2 * n] = fma(gv.x, s1, rs[1][2 * n]);
+            rs[1][2 * n + 1] = fma(gv.y, s1, rs[1][2 * n + 1]);
+        }
+    }
     double quad[2] = {0.0, 0.0}, lin[2] = {0.0, 0.0}, tr = 0.0;
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
 #pragma unroll
         for (int dl = 0; dl < 2; ++dl) {
             const int i = 8 * n + 2 * t + dl;
-            const double* Gi = G + (int64_t)i * N;
-            double rs0 = 0.0, rs1 = 0.0;
-            for (int j = 0; j < N; j += 2) {
-                const double2 gij = __ldg(reinterpret_cast<const double2*>(Gi + j));
-                const double s00 = (double)((int)((pos[0] >> j) & 1u) - (int)((neg[0] >> j) & 1u));
-                const double s01 = (double)((int)((pos[0] >> (j + 1)) & 1u) - (int)((neg[0] >> (j + 1)) & 1u));
-                const double s10 = (double)((int)((pos[1] >> j) & 1u) - (int)((neg[1] >> j) & 1u));
-                const double s11 = (double)((int)((pos[1] >> (j + 1)) & 1u) - (int)((neg[1] >> (j + 1)) & 1u));
-                rs0 = fma(gij.x, s00, rs0);
-                rs0 = fma(gij.y, s01, rs0);
-                rs1 = fma(gij.x, s10, rs1);
-                rs1 = fma(gij.y, s11, rs1);
-            }
             const double si0 = (double)((int)((pos[0] >> i) & 1u) - (int)((neg[0] >> i) & 1u));
             const double si1 = (double)((int)((pos[1] >> i) & 1u) - (int)((neg[1] >> i) & 1u));
-            quad[0] = fma(si0, rs0, quad[0]);
-            quad[1] = fma(si1, rs1, quad[1]);
+            quad[0] = fma(si0, rs[0][2 * n + dl], quad[0]);
+            quad[1] = fma(si1, rs[1][2 * n + dl], quad[1]);
             const double bi = __ldg(bg + i);
             lin[0] = fma(bi, si0, lin[0]);
             lin[1] = fma(bi, si1, lin[1]);
-            tr += __ldg(Gi + i);
+            tr += __ldg(G + (int64_t)i * N + i);
         }
     }
 #pragma unroll
