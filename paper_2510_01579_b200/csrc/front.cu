@@ -247,26 +247,18 @@ __device__ void load_problem(const double* Hg, const double* yg, int64_t prob, i
 
 // r = y - H x_g (x_g from level indices), returns ||r||^2 on every lane.
 __device__ double residual_from_idx(const cplx* H, const cplx* y, const uint8_t* idx, int n_r,
-                                    int n_t, const Alphabet& al, cplx* r, int lane) {
+                                    int n_t, const Alphabet& al, cplx* r, cplx* xs, int lane) {
+    for (int j = lane; j < n_t; j += 32) xs[j] = {al.levels[idx[2 * j]], al.levels[idx[2 * j + 1]]};
+    __syncwarp();
     double acc = 0.0;
     for (int k = lane; k < n_r; k += 32) {
-        cplx s = {0.0, 0.0};
-        for (int j = 0; j < n_t; ++j) {
-            const cplx xj = {al.levels[idx[2 * j]], al.levels[idx[2 * j + 1]]};
-            s = cadd(s, cmul(H[k * n_t + j], xj));
-        }
-        const cplx rk = csub(y[k], s);
+        const cplx rk = resid_row(H + k * n_t, xs, n_t, y[k]);
         r[k] = rk;
-        acc += cabs2(rk);
+        acc = __dadd_rn(acc, abs2_rn(rk));
     }
     __syncwarp();
     return warp_sum(acc);
 }
-
-struct IsingOut {
-    double *G, *g, *b, *offset, *eps_scale, *eps_out;
-    double eps_gain, fixed_eps;
-};
 
 // G, g_diag, b, offset, eps_scale around the guess whose residual is r (r2 = ||r||^2).
 __device__ void emit_ising(cplx* H, const cplx* r, double r2, cplx* A, cplx* scr, int n_r, int n_t,
@@ -353,7 +345,7 @@ __global__ void k_front(const double* __restrict__ Hg, const double* __restrict_
         }
         __syncwarp();
     }
-    const double r2 = residual_from_idx(sm.H, sm.y, idx, n_r, n_t, al, sm.r, lane);
+    const double r2 = residual_from_idx(sm.H, sm.y, idx, n_r, n_t, al, sm.r, sm.scr, lane);
     if (energy && lane == 0) energy[prob] = r2;
     if (DO_ISING) emit_ising(sm.H, sm.r, r2, sm.A, sm.scr, n_r, n_t, al, prob, o, lane);
 }
@@ -390,8 +382,11 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
     cplx* H = reinterpret_cast<cplx*>(b + N);
     cplx* y = H + n_r * n_t;
     const double* Gp = Gg + prob * (int64_t)N * N;
-    for (int i = lane; i < N * N; i += 32) G[i] = Gp[i];
-    for (int i = lane; i < N; i += 32) b[i] = bg[prob * N + i];
+    // G and b are only needed when the anneal kernel did not supply energies
+    if (!energies) {
+        for (int i = lane; i < N * N; i += 32) G[i] = Gp[i];
+        for (int i = lane; i < N; i += 32) b[i] = bg[prob * N + i];
+    }
     {
         const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n_t;
         for (int i = lane; i < n_r * n_t; i += 32) H[i] = Hp[i];
@@ -400,7 +395,8 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
     }
     double gsum = 0.0;
     __syncwarp();
-    for (int i = 0; i < N; ++i) gsum += G[i * N + i];
+    if (!energies)
+        for (int i = 0; i < N; ++i) gsum += G[i * N + i];
 
     // energies: lane = anneal, E = u'Gu - 2 tr G + 2 s_aux b'u  (solver.py:171-175)
     double best_e = INFINITY;
@@ -452,6 +448,7 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
     bool take = false;
     double e_dec = 0.0;
     __shared__ uint8_t cand_all[8][128];
+    __shared__ cplx xs_all[8][64];
     uint8_t* cand = cand_all[warp];
     if (best_i >= 0 && !(best_e + offset[prob] > e_guess)) {
         const int8_t* s = sp0 + (int64_t)best_i * S;
@@ -465,15 +462,12 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
         }
         __syncwarp();
         // residual of the decoded vector (linear.py:44-47)
+        cplx* xs = xs_all[warp];
+        for (int j = lane; j < n_t; j += 32) xs[j] = {al.levels[cand[2 * j]], al.levels[cand[2 * j + 1]]};
+        __syncwarp();
         double acc = 0.0;
-        for (int k = lane; k < n_r; k += 32) {
-            cplx sacc = {0.0, 0.0};
-            for (int j = 0; j < n_t; ++j) {
-                const cplx xj = {al.levels[cand[2 * j]], al.levels[cand[2 * j + 1]]};
-                sacc = cadd(sacc, cmul(H[k * n_t + j], xj));
-            }
-            acc += cabs2(csub(y[k], sacc));
-        }
+        for (int k = lane; k < n_r; k += 32)
+            acc = __dadd_rn(acc, abs2_rn(resid_row(H + k * n_t, xs, n_t, y[k])));
         e_dec = warp_sum(acc);
         take = e_dec < e_guess;
     }
@@ -651,12 +645,15 @@ int launch_mmse(const double* H, const double* y, const double* noise_var, int64
                 int n_t, const Alphabet& al, uint8_t* x_idx, double* energy, int8_t* status,
                 cudaStream_t st) {
     if (P == 0) return IL_OK;
+    IsingOut o{};
+    if (front_rows_supported(n_r, n_t))
+        return launch_front_rows(true, false, H, y, noise_var, P, n_r, n_t, al, x_idx, energy,
+                                 status, o, st);
     int wpb;
     size_t smem;
     const int blocks = front_blocks(P, FrontSmem::bytes(n_r, n_t), &wpb, &smem);
     int rc = set_smem((const void*)k_front<true, false>, smem);
     if (rc) return rc;
-    IsingOut o{};
     IL_LAUNCH(kProfFront, st, k_front<true, false><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
                                                           energy, status, o););
     IL_CHECK_CUDA(cudaGetLastError());
@@ -668,12 +665,15 @@ int launch_build_ising(const double* H, const double* y, const uint8_t* guess_id
                        double* b, double* offset, double* eps_scale, double* eps_out,
                        double eps_gain, double fixed_eps, cudaStream_t st) {
     if (P == 0) return IL_OK;
+    IsingOut o{G, g_diag, b, offset, eps_scale, eps_out, eps_gain, fixed_eps};
+    if (front_rows_supported(n_r, n_t))
+        return launch_front_rows(false, true, H, y, nullptr, P, n_r, n_t, al,
+                                 const_cast<uint8_t*>(guess_idx), nullptr, nullptr, o, st);
     int wpb;
     size_t smem;
     const int blocks = front_blocks(P, FrontSmem::bytes(n_r, n_t), &wpb, &smem);
     int rc = set_smem((const void*)k_front<false, true>, smem);
     if (rc) return rc;
-    IsingOut o{G, g_diag, b, offset, eps_scale, eps_out, eps_gain, fixed_eps};
     IL_LAUNCH(kProfFront, st, k_front<false, true><<<blocks, 32 * wpb, smem, st>>>(H, y, nullptr, P, n_r, n_t, al,
                                                           const_cast<uint8_t*>(guess_idx),
                                                           nullptr, nullptr, o););
@@ -686,12 +686,15 @@ int launch_mmse_ising(const double* H, const double* y, const double* noise_var,
                       int8_t* status, double* G, double* g_diag, double* b, double* offset,
                       double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st) {
     if (P == 0) return IL_OK;
+    IsingOut o{G, g_diag, b, offset, nullptr, eps_out, eps_gain, fixed_eps};
+    if (front_rows_supported(n_r, n_t))
+        return launch_front_rows(true, true, H, y, noise_var, P, n_r, n_t, al, x_idx, energy,
+                                 status, o, st);
     int wpb;
     size_t smem;
     const int blocks = front_blocks(P, FrontSmem::bytes(n_r, n_t), &wpb, &smem);
     int rc = set_smem((const void*)k_front<true, true>, smem);
     if (rc) return rc;
-    IsingOut o{G, g_diag, b, offset, nullptr, eps_out, eps_gain, fixed_eps};
     IL_LAUNCH(kProfFront, st, k_front<true, true><<<blocks, 32 * wpb, smem, st>>>(H, y, noise_var, P, n_r, n_t, al, x_idx,
                                                          energy, status, o););
     IL_CHECK_CUDA(cudaGetLastError());

@@ -39,10 +39,26 @@ IL_HD cplx cadd(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
 IL_HD cplx csub(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
 IL_HD double cabs2(cplx a) { return a.re * a.re + a.im * a.im; }
 
+// Residual row r_k = y_k - sum_j H[k][j] x_j with every operation rounded
+// explicitly (no contraction choices left to the compiler), so that every
+// kernel computing ||y - Hx||^2 (linear.py:44-47) agrees bit-for-bit: the
+// guess energy and the decoded-vector energy must tie exactly when the
+// decision is unchanged (strict test, detector.py:52).
+IL_D cplx resid_row(const cplx* Hk, const cplx* x, int n, cplx yk) {
+    double sr = 0.0, si = 0.0;
+    for (int j = 0; j < n; ++j) {
+        const cplx a = Hk[j], b = x[j];
+        sr = __dadd_rn(sr, __fma_rn(a.re, b.re, -__dmul_rn(a.im, b.im)));
+        si = __dadd_rn(si, __fma_rn(a.re, b.im, __dmul_rn(a.im, b.re)));
+    }
+    return {__dsub_rn(yk.re, sr), __dsub_rn(yk.im, si)};
+}
+IL_D double abs2_rn(cplx a) { return __fma_rn(a.re, a.re, __dmul_rn(a.im, a.im)); }
+
 // ---- warp helpers ----------------------------------------------------------
 IL_D double warp_sum(double v) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 

@@ -31,6 +31,17 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
 
 // ---- front-end / reduction kernels -----------------------------------------
+// Ising outputs of the front-end kernels (any pointer may be null).
+struct IsingOut {
+    double *G, *g, *b, *offset, *eps_scale, *eps_out;
+    double eps_gain, fixed_eps;
+};
+// Register-resident front-end for n_t <= 16 (front_rows.cu).
+bool front_rows_supported(int n_r, int n_t);
+int launch_front_rows(bool do_mmse, bool do_ising, const double* H, const double* y,
+                      const double* s2, int64_t P, int n_r, int n_t, const Alphabet& al,
+                      uint8_t* x_idx, double* energy, int8_t* status, const IsingOut& o,
+                      cudaStream_t st);
 int launch_mmse(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
                 int n_t, const Alphabet& al, uint8_t* x_idx, double* energy, int8_t* status,
                 cudaStream_t st);
