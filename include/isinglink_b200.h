@@ -155,6 +155,20 @@ int il_detect_cim_batch(const double* H, const double* y, const double* noise_va
                         int32_t* diverged_count, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Host-buffer form of il_detect_cim_batch: every pointer is HOST memory (the
+ * numpy-in / numpy-out shape of the reference's detect_cim over a slot).
+ * The slot is streamed through the device in n_chunks pieces (<= 0: auto)
+ * with the H2D copy, the detection and the D2H copy of consecutive chunks
+ * overlapped on separate streams; returns when the outputs are in host
+ * memory.  Pinned (page-locked) host buffers are needed for the overlap.
+ * ------------------------------------------------------------------------- */
+int il_detect_cim_host(const double* H, const double* y, const double* noise_var,
+                       int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                       const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
+                       double* energy, int8_t* source, int32_t* anneal_index,
+                       int32_t* diverged_count, int32_t n_chunks);
+
+/* ---------------------------------------------------------------------------
  * Batched downlink vector-perturbation precoding: P x precode_vpp
  * (precoder.py:93-146).  H [P, n_u, n_ant] complex128 (n_u <= n_ant),
  * u [P, n_u] complex128 symbols, power P_tot > 0, tau, n_stages >= 1,

@@ -90,6 +90,53 @@ def detect_cim_batch(H, y, noise_var, order: int, seeds, params=None,
     return out
 
 
+def _host(x, dtype: torch.dtype, shape) -> torch.Tensor:
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(x))
+    if t.device.type != "cpu":
+        raise ValueError("detect_cim_host takes host (CPU) buffers")
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    t = t.contiguous()
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
+def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
+                    precision: str | None = None, n_chunks: int = 0, out=None) -> DetectBatch:
+    """P x ``detect_cim`` from HOST buffers to HOST buffers.
+
+    The slot is streamed through the GPU in chunks with H2D copy, detection
+    and D2H copy overlapped (il_detect_cim_host).  Pass pinned CPU tensors
+    (``tensor.pin_memory()``) for the overlap; ``out`` may hold preallocated
+    (pinned) output tensors in DetectBatch layout."""
+    params = params or CacParams()
+    prm = to_c(params, precision)
+    Ht = H if isinstance(H, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(H))
+    if Ht.dim() != 3:
+        raise ValueError("H must be [P, n_r, n_t]")
+    P, n_r, n_t = Ht.shape
+    Hh = _host(Ht, torch.complex128, (P, n_r, n_t))
+    yh = _host(y, torch.complex128, (P, n_r))
+    sh = _host(noise_var, torch.float64, (P,))
+    st = seeds if isinstance(seeds, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1)))
+    if st.dtype not in (torch.uint64, torch.int64):
+        raise TypeError("seeds must be uint64 (or int64 bit patterns)")
+    st = _host(st, st.dtype, (P,))
+    if out is None:
+        out = DetectBatch(x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8),
+                          energy=torch.empty(P, dtype=torch.float64),
+                          source=torch.empty(P, dtype=torch.int8),
+                          anneal_index=torch.empty(P, dtype=torch.int32),
+                          diverged=torch.empty(P, dtype=torch.int32))
+    _lib.call("il_detect_cim_host", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(), P, n_r, n_t,
+              int(order), st.data_ptr(), prm, out.x_idx.data_ptr(), out.energy.data_ptr(),
+              out.source.data_ptr(), out.anneal_index.data_ptr(), out.diverged.data_ptr(),
+              int(n_chunks))
+    return out
+
+
 @dataclass
 class PrecodeBatch:
     x: torch.Tensor              # complex128 [P, n_ant] power-normalised transmit vector

@@ -189,3 +189,38 @@ def test_oracle_agrees_on_random_instances():
         r = batched.detect_cim_batch(np.array(Hs), np.array(ys), np.array(s2s), order,
                                      np.array(seeds, np.uint64), CacParams(precision="fp64_exact"))
         assert np.array_equal(r.x_idx.cpu().numpy(), np.array(want))
+
+
+@pytest.mark.parametrize("n_chunks", [0, 1, 3, 7])
+def test_detect_cim_host_pipeline_matches_device_batch(n_chunks):
+    """The chunked host-buffer pipeline (il_detect_cim_host) returns exactly
+    what the device-resident batch returns, for any chunking (ragged last
+    chunk included), and matches the reference fixtures."""
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    d = load_golden("d16x16_16qam_20db.npz")
+    reps = 5  # tile the fixture to a ragged multi-chunk batch
+    H = np.concatenate([d["H"]] * reps)[:-3]
+    y = np.concatenate([d["y"]] * reps)[:-3]
+    s2 = np.concatenate([d["noise_var"]] * reps)[:-3]
+    seed = np.concatenate([d["seed"]] * reps)[:-3]
+    for prec in ("fp64_exact", "fp32"):
+        prm = CacParams(precision=prec)
+        dev = batched.detect_cim_batch(H, y, s2, int(d["order"]), seed, prm)
+        host = batched.detect_cim_host(torch.from_numpy(H).pin_memory(),
+                                       torch.from_numpy(y).pin_memory(),
+                                       torch.from_numpy(s2).pin_memory(),
+                                       int(d["order"]), seed, prm, n_chunks=n_chunks)
+        for f in ("x_idx", "energy", "source", "anneal_index", "diverged"):
+            assert torch.equal(getattr(dev, f).cpu(), getattr(host, f)), (prec, f)
+        if prec == "fp64_exact":
+            n = len(d["x_hat"])
+            assert np.array_equal(host.x_idx.numpy()[:n], d["x_hat"])
+
+
+def test_detect_cim_host_rejects_device_buffers():
+    from paper_2510_01579_b200 import batched
+    H = torch.zeros((2, 4, 4), dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError):
+        batched.detect_cim_host(H, torch.zeros((2, 4), dtype=torch.complex128),
+                                torch.ones(2, dtype=torch.float64), 4, np.arange(2, dtype=np.uint64))
