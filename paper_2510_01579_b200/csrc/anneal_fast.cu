@@ -49,6 +49,9 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_FAST_MINB
 #define IL_FAST_MINB 3
 #endif
+#ifndef IL_LOOP2  // refresh-period outer loop, f_mvm Euler steps inner
+#define IL_LOOP2 0
+#endif
 
 struct FastScalars {
     float alpha;    // 1 + dt (p - 1)
@@ -242,10 +245,15 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     }
     __syncwarp();
 
+#if IL_LOOP2
+    for (int step0 = 0; step0 < s.n_steps; step0 += s.f_mvm) {
+        {
+#else
     int until_refresh = 0;
     for (int step = 0; step < s.n_steps; ++step) {
         if (until_refresh == 0) {
             until_refresh = s.f_mvm;
+#endif
             // ---- refresh: v = x1 + x2, M' = -Ks G v on tensor cores -----------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
@@ -324,6 +332,11 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 }
             }
         }
+#if IL_LOOP2
+        const int n_in = min(s.f_mvm, s.n_steps - step0);
+#pragma unroll 2
+        for (int k = 0; k < n_in; ++k) {
+#endif
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -333,7 +346,11 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             }
         }
         euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
+#if IL_LOOP2
+        }
+#else
         --until_refresh;
+#endif
     }
 
     // ---- epilogue: divergence flags, spins, FP64 energies --------------------
