@@ -154,5 +154,57 @@ def main():
     print("golden fixtures written to", HERE)
 
 
+def main_multi():
+    """MMGaP-E (detect_cim_multi, detector.py:85-134), MMSE-SIC
+    (linear.py:78-106) and brute-force ML (linear.py:109-144) fixtures."""
+    il = import_reference()
+    from isinglink.harness.config import ExperimentConfig
+    from isinglink.harness.sweeps import make_uplink_instance
+    sets = [  # name, n_r, n_t, order, snr, n_trials, n_stages
+        ("m8x8_16qam_15db", 8, 8, 16, 15.0, 48, 2),
+        ("m16x16_16qam_20db", 16, 16, 16, 20.0, 32, 1),
+    ]
+    src_code = {"mmse": 0, "anneal": 1, "mmse_sic": 2}
+    for name, nr, nt, order, snr, ntr, ns in sets:
+        cfg = ExperimentConfig(n_r=nr, n_t=nt, modulation=order, snr_grid_db=(snr,),
+                               n_trials=ntr, seed=3)
+        levels = il.make_qam(order).pam_levels
+        rec = {k: [] for k in ("H", "y", "noise_var", "seed", "x_sic", "e_sic", "x_hat",
+                               "energy", "source", "anneal_index", "diverged")}
+        for t in range(ntr):
+            inst = make_uplink_instance(cfg, 0, t)
+            seed = il.derive_seed(cfg.seed, 1, 0, t, 3)
+            sic = il.detect_mmse_sic(inst)
+            r = il.detect_cim_multi(inst, cfg.cac, n_stages=ns, seed=seed)
+            rec["H"].append(inst.H); rec["y"].append(inst.y); rec["noise_var"].append(inst.noise_var)
+            rec["seed"].append(seed)
+            rec["x_sic"].append(level_idx(sic.x_hard, levels)); rec["e_sic"].append(sic.energy)
+            rec["x_hat"].append(level_idx(r.x_hard, levels)); rec["energy"].append(r.energy)
+            rec["source"].append(src_code[r.source]); rec["anneal_index"].append(r.anneal_index)
+            rec["diverged"].append(r.diverged_count)
+        out = {k: np.array(v) for k, v in rec.items() if k != "seed"}
+        out["seed"] = np.array(rec["seed"], dtype=np.uint64)  # 64-bit ints, no float detour
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), order=order, n_stages=ns, **out)
+    # brute-force ML (small search spaces)
+    specs = [("ml4x4_qpsk_8db", 4, 4, 4, 8.0, 24), ("ml3x2_16qam_12db", 3, 2, 16, 12.0, 24)]
+    for name, nr, nt, order, snr, ntr in specs:
+        cfg = ExperimentConfig(n_r=nr, n_t=nt, modulation=order, snr_grid_db=(snr,),
+                               n_trials=ntr, seed=4)
+        levels = il.make_qam(order).pam_levels
+        Hs, ys, xs, es = [], [], [], []
+        for t in range(ntr):
+            inst = make_uplink_instance(cfg, 0, t)
+            r = il.detect_ml(inst)
+            Hs.append(inst.H); ys.append(inst.y)
+            xs.append(level_idx(r.x_hard, levels)); es.append(r.energy)
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), H=np.array(Hs), y=np.array(ys),
+                            x_ml=np.array(xs), e_ml=np.array(es), order=order)
+    print("MMGaP-E / SIC / ML fixtures written to", HERE)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "multi":
+        main_multi()
+    else:
+        main()
+        main_multi()

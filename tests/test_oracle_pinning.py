@@ -114,3 +114,50 @@ def test_gray_and_bit_errors():
     a = np.array([[0, 1], [3, 2]])
     assert orc.bit_errors(a, a) == 0
     assert orc.bit_errors(np.array([[0, 0]]), np.array([[1, 0]])) == 1
+
+
+MULTI_SETS = ["m8x8_16qam_15db", "m16x16_16qam_20db"]
+_SRC = {"mmse": 0, "anneal": 1, "mmse_sic": 2}
+
+
+@pytest.mark.parametrize("name", MULTI_SETS)
+def test_oracle_mmse_sic_matches_reference(name):
+    """linear.py:78-106 restatement against the reference's detect_mmse_sic."""
+    d = load_golden(f"{name}.npz")
+    levels, _ = orc.qam(int(d["order"]))
+    for i in range(len(d["H"])):
+        x, e = orc.mmse_sic(d["H"][i], d["y"][i], float(d["noise_var"][i]), levels)
+        idx = np.stack([orc.level_index(x.real, levels), orc.level_index(x.imag, levels)], -1)
+        assert np.array_equal(idx, d["x_sic"][i])
+        assert e == d["e_sic"][i]
+
+
+@pytest.mark.parametrize("name", MULTI_SETS)
+def test_oracle_detect_cim_multi_matches_reference(name):
+    """detector.py:85-134 restatement against the reference's detect_cim_multi."""
+    d = load_golden(f"{name}.npz")
+    order = int(d["order"])
+    levels, _ = orc.qam(order)
+    n = 12 if "16x16" in name else len(d["H"])  # keep the CPU suite short
+    for i in range(n):
+        r = orc.detect_cim_multi(d["H"][i], d["y"][i], float(d["noise_var"][i]), order,
+                                 n_stages=int(d["n_stages"]), seed=int(d["seed"][i]))
+        idx = np.stack([orc.level_index(r["x"].real, levels),
+                        orc.level_index(r["x"].imag, levels)], -1)
+        assert np.array_equal(idx, d["x_hat"][i]), i
+        assert r["energy"] == d["energy"][i]
+        assert _SRC[r["source"]] == d["source"][i]
+        assert r["anneal_index"] == d["anneal_index"][i]
+        assert r["diverged"] == d["diverged"][i]
+
+
+@pytest.mark.parametrize("name", ["ml4x4_qpsk_8db", "ml3x2_16qam_12db"])
+def test_oracle_ml_matches_reference(name):
+    """linear.py:109-144 restatement against the reference's detect_ml."""
+    d = load_golden(f"{name}.npz")
+    levels, _ = orc.qam(int(d["order"]))
+    for i in range(len(d["H"])):
+        x, e = orc.ml(d["H"][i], d["y"][i], levels)
+        idx = np.stack([orc.level_index(x.real, levels), orc.level_index(x.imag, levels)], -1)
+        assert np.array_equal(idx, d["x_ml"][i])
+        assert e == d["e_ml"][i]
