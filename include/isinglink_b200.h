@@ -59,8 +59,11 @@ typedef struct il_cac_params {
     double init_amplitude;    /*                                       (0.1)  */
 } il_cac_params;
 
-/* Per-problem outcome of a batched detection (DetectionResult, linear.py:33-41). */
-enum il_source { IL_SRC_GUESS = 0, IL_SRC_ANNEAL = 1, IL_SRC_FAILED = -1 };
+/* Per-problem outcome of a batched detection (DetectionResult.source,
+ * linear.py:33-41): "mmse" (the guess) = 0, "anneal" = 1, "mmse_sic" = 2
+ * (detect_cim_multi only), -1 = the baseline's Cholesky failed (the
+ * reference raises LinAlgError there). */
+enum il_source { IL_SRC_GUESS = 0, IL_SRC_ANNEAL = 1, IL_SRC_SIC = 2, IL_SRC_FAILED = -1 };
 
 const char* il_last_error(void);
 int il_abi_version(void);
@@ -153,6 +156,31 @@ int il_detect_cim_batch(const double* H, const double* y, const double* noise_va
                         const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
                         double* energy, int8_t* source, int32_t* anneal_index,
                         int32_t* diverged_count, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * MMGaP-E (detector.py:85-134, linear.py:78-106).
+ *   il_mmse_sic_batch — P x detect_mmse_sic: x_idx[P*n_t*2] level indices,
+ *     energy[P] residual, status[P] (0 ok, -1 Cholesky failure).
+ *   il_detect_cim_multi_batch — P x detect_cim_multi(inst, params, n_stages,
+ *     seed[p], chains): chains[n_chains] are chain codes in order
+ *     (0 = "mmse", 1 = "mmse_sic"; the reference default is {0, 1});
+ *     chain c, stage s anneals with derive_seed(seed[p], c, s).  Outputs as
+ *     il_detect_cim_batch with source in {0 mmse, 1 anneal, 2 mmse_sic};
+ *     diverged_count[P] sums every chain and stage.
+ * ------------------------------------------------------------------------- */
+/* ||y - H x||^2 per problem (linear.py:44-47) for complex128 x[P*n_t]; the
+ * same arithmetic as every energy the detectors compute. */
+int il_residual_batch(const double* H, const double* y, const double* x, int64_t P,
+                      int32_t n_r, int32_t n_t, double* energy, void* stream);
+int il_mmse_sic_batch(const double* H, const double* y, const double* noise_var, int64_t P,
+                      int32_t n_r, int32_t n_t, int32_t qam_order, uint8_t* x_idx,
+                      double* energy, int8_t* status, void* stream);
+int il_detect_cim_multi_batch(const double* H, const double* y, const double* noise_var,
+                              int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                              const uint64_t* seed, const il_cac_params* prm,
+                              int32_t n_stages, const int32_t* chains, int32_t n_chains,
+                              uint8_t* x_idx, double* energy, int8_t* source,
+                              int32_t* anneal_index, int32_t* diverged_count, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Host-buffer form of il_detect_cim_batch: every pointer is HOST memory (the

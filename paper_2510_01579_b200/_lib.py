@@ -49,6 +49,12 @@ _SIGS = {
     "il_detect_cim_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
                              ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _vp],
                             ctypes.c_int),
+    "il_residual_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _vp, _vp], ctypes.c_int),
+    "il_mmse_sic_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp],
+                          ctypes.c_int),
+    "il_detect_cim_multi_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
+                                   ctypes.POINTER(CacParamsC), _c_i32, _vp, _c_i32, _vp, _vp,
+                                   _vp, _vp, _vp, _vp], ctypes.c_int),
     "il_detect_cim_host": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
                             ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _c_i32],
                            ctypes.c_int),

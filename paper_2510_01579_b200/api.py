@@ -120,9 +120,13 @@ def _note(counters, diverged, steps, mvms):
 
 
 def residual_energy(H: np.ndarray, y: np.ndarray, x: np.ndarray) -> float:
-    """||y - Hx||^2 (linear.py:44-47)."""
-    r = np.asarray(y) - np.asarray(H) @ np.asarray(x)
-    return float(np.real(np.vdot(r, r)))
+    """||y - Hx||^2 (linear.py:44-47) on the GPU, in the same arithmetic as
+    the energies the detectors compute, so guess and decoded energies tie
+    exactly when the decision is unchanged (strict test, detector.py:52)."""
+    H = np.asarray(H, dtype=np.complex128)
+    y = np.asarray(y, dtype=np.complex128)
+    x = np.asarray(x, dtype=np.complex128)
+    return float(batched.residual_batch(H[None], y[None], x[None])[0])
 
 
 # ---------------------------------------------------------------------------
@@ -139,6 +143,19 @@ def detect_mmse(inst: MimoInstance) -> DetectionResult:
         raise np.linalg.LinAlgError("regularized normal matrix is not positive definite")
     x = from_indices(x_idx[0].cpu().numpy(), inst.constellation)
     return DetectionResult(x_hard=x, energy=float(energy[0]), source="mmse")
+
+
+def detect_mmse_sic(inst: MimoInstance) -> DetectionResult:
+    """linear.py:78-106 (ordered MMSE-SIC) on the GPU."""
+    if inst.n_r < inst.n_t:
+        raise ValueError("uplink detection requires n_r >= n_t")
+    x_idx, energy, status = batched.mmse_sic_batch(inst.H[None], inst.y[None],
+                                                   np.array([inst.noise_var]),
+                                                   _order_code(inst.constellation))
+    if int(status[0]) != 0:
+        raise np.linalg.LinAlgError("regularized normal matrix is not positive definite")
+    x = from_indices(x_idx[0].cpu().numpy(), inst.constellation)
+    return DetectionResult(x_hard=x, energy=float(energy[0]), source="mmse_sic")
 
 
 def build_ising(inst: MimoInstance, x_guess: np.ndarray) -> StructuredIsing:
@@ -281,6 +298,55 @@ def detect_cim(inst: MimoInstance, params=None, seed: int = 0, counters=None) ->
     x = from_indices(r.x_idx[0].cpu().numpy(), inst.constellation)
     return DetectionResult(x_hard=x, energy=float(r.energy[0]),
                            source="anneal" if src == 1 else "mmse",
+                           anneal_index=int(r.anneal_index[0]),
+                           diverged_count=int(r.diverged[0]))
+
+
+_SOURCES = {0: "mmse", 1: "anneal", 2: "mmse_sic"}
+
+
+def detect_cim_multi(inst: MimoInstance, params=None, n_stages: int = 1, seed: int = 0,
+                     chains: tuple = ("mmse", "mmse_sic"), counters=None,
+                     stage_log: list | None = None) -> DetectionResult:
+    """MMGaP-E, detector.py:85-134: one fused batched call (P = 1).
+
+    ``counters`` / ``stage_log`` are the reference's instrumentation hooks;
+    with either given the chains run stage by stage through the per-stage
+    API so the hooks see every stage."""
+    params = params or CacParams()
+    if n_stages < 1:
+        raise ValueError("n_stages must be >= 1")
+    if counters is not None or stage_log is not None:
+        fns = {"mmse": detect_mmse, "mmse_sic": detect_mmse_sic}
+        baselines = [(name, fns[name](inst)) for name in chains]
+        best = min(baselines, key=lambda kv: kv[1].energy)[1]
+        total = 0
+        for chain_id, (name, base) in enumerate(baselines):
+            guess, energy, widx = base.x_hard, base.energy, -1
+            for stage in range(n_stages):
+                guess, energy, idx, div = _improve_guess(inst, guess, energy, params,
+                                                         derive_seed(seed, chain_id, stage),
+                                                         counters)
+                total += div
+                if idx >= 0:
+                    widx = idx
+                if stage_log is not None:
+                    stage_log.append((name, stage, energy))
+            if energy < best.energy:
+                best = DetectionResult(x_hard=guess, energy=energy, source="anneal",
+                                       anneal_index=widx)
+        return DetectionResult(x_hard=best.x_hard, energy=best.energy, source=best.source,
+                               anneal_index=best.anneal_index, diverged_count=total)
+    if inst.n_r < inst.n_t:
+        raise ValueError("uplink detection requires n_r >= n_t")
+    r = batched.detect_cim_multi_batch(inst.H[None], inst.y[None], np.array([inst.noise_var]),
+                                       _order_code(inst.constellation),
+                                       np.array([seed], np.uint64), params, n_stages, chains)
+    src = int(r.source[0])
+    if src < 0:
+        raise np.linalg.LinAlgError("regularized normal matrix is not positive definite")
+    x = from_indices(r.x_idx[0].cpu().numpy(), inst.constellation)
+    return DetectionResult(x_hard=x, energy=float(r.energy[0]), source=_SOURCES[src],
                            anneal_index=int(r.anneal_index[0]),
                            diverged_count=int(r.diverged[0]))
 

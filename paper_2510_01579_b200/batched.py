@@ -184,6 +184,68 @@ def mmse_batch(H, y, noise_var, order: int):
     return x_idx, energy, status
 
 
+def residual_batch(H, y, x) -> torch.Tensor:
+    """||y - H x||^2 per problem (linear.py:44-47), x complex [P, n_t]."""
+    Hd = _dev(H, torch.complex128)
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    xd = _dev(x, torch.complex128)
+    out = torch.empty(P, dtype=torch.float64, device=Hd.device)
+    _lib.call("il_residual_batch", Hd.data_ptr(), yd.data_ptr(), xd.data_ptr(), P, n_r, n_t,
+              out.data_ptr(), _stream())
+    return out
+
+
+def mmse_sic_batch(H, y, noise_var, order: int):
+    """P x ``detect_mmse_sic`` (linear.py:78-106) -> (x_idx, energy, status)."""
+    Hd = _dev(H, torch.complex128)
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    sd = _dev(noise_var, torch.float64)
+    x_idx = torch.empty((P, n_t, 2), dtype=torch.uint8, device=Hd.device)
+    energy = torch.empty(P, dtype=torch.float64, device=Hd.device)
+    status = torch.empty(P, dtype=torch.int8, device=Hd.device)
+    _lib.call("il_mmse_sic_batch", Hd.data_ptr(), yd.data_ptr(), sd.data_ptr(), P, n_r, n_t,
+              int(order), x_idx.data_ptr(), energy.data_ptr(), status.data_ptr(), _stream())
+    return x_idx, energy, status
+
+
+CHAIN_CODES = {"mmse": 0, "mmse_sic": 1}
+
+
+def detect_cim_multi_batch(H, y, noise_var, order: int, seeds, params=None, n_stages: int = 1,
+                           chains=("mmse", "mmse_sic"),
+                           precision: str | None = None) -> DetectBatch:
+    """P x ``detect_cim_multi`` (MMGaP-E, detector.py:85-134).
+
+    ``source``: 0 mmse, 1 anneal, 2 mmse_sic, -1 failed baseline."""
+    params = params or CacParams()
+    prm = to_c(params, precision)
+    if n_stages < 1:
+        raise ValueError("n_stages must be >= 1")
+    codes = np.array([CHAIN_CODES[c] for c in chains], dtype=np.int32)
+    Hd = _dev(H, torch.complex128)
+    if Hd.dim() != 3:
+        raise ValueError("H must be [P, n_r, n_t]")
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    sd = _dev(noise_var, torch.float64)
+    seed_t = _seeds(seeds, P)
+    dev = Hd.device
+    out = DetectBatch(
+        x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8, device=dev),
+        energy=torch.empty(P, dtype=torch.float64, device=dev),
+        source=torch.empty(P, dtype=torch.int8, device=dev),
+        anneal_index=torch.empty(P, dtype=torch.int32, device=dev),
+        diverged=torch.empty(P, dtype=torch.int32, device=dev),
+    )
+    _lib.call("il_detect_cim_multi_batch", Hd.data_ptr(), yd.data_ptr(), sd.data_ptr(), P, n_r,
+              n_t, int(order), seed_t.data_ptr(), prm, int(n_stages), codes.ctypes.data,
+              len(codes), out.x_idx.data_ptr(), out.energy.data_ptr(), out.source.data_ptr(),
+              out.anneal_index.data_ptr(), out.diverged.data_ptr(), _stream())
+    return out
+
+
 def build_ising_batch(H, y, guess_idx, order: int) -> dict:
     """P x ``build_ising`` (transform.py:108-140) around level-index guesses.
 

@@ -277,6 +277,111 @@ int il_detect_cim_batch(const double* H, const double* y, const double* noise_va
                              anneal_index, diverged_count, ws, st);
 }
 
+int il_residual_batch(const double* H, const double* y, const double* x, int64_t P, int32_t n_r,
+                      int32_t n_t, double* energy, void* stream) {
+    IL_REQUIRE(P >= 0 && n_r >= 1 && n_t >= 1, "invalid shape");
+    return launch_residual(H, y, x, P, n_r, n_t, energy, (cudaStream_t)stream);
+}
+
+int il_mmse_sic_batch(const double* H, const double* y, const double* noise_var, int64_t P,
+                      int32_t n_r, int32_t n_t, int32_t qam_order, uint8_t* x_idx, double* energy,
+                      int8_t* status, void* stream) {
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
+               "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
+    IL_REQUIRE(P == 0 || x_idx, "x_idx must not be NULL");
+    Alphabet al;
+    int rc = make_qam_alphabet(qam_order, &al);
+    if (rc) return rc;
+    return launch_mmse_sic(H, y, noise_var, P, n_r, n_t, al, x_idx, energy, status,
+                           (cudaStream_t)stream);
+}
+
+int il_detect_cim_multi_batch(const double* H, const double* y, const double* noise_var,
+                              int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                              const uint64_t* seed, const il_cac_params* prm, int32_t n_stages,
+                              const int32_t* chains, int32_t n_chains, uint8_t* x_idx,
+                              double* energy, int8_t* source, int32_t* anneal_index,
+                              int32_t* diverged_count, void* stream) {
+    int rc = validate(prm);
+    if (rc) return rc;
+    IL_REQUIRE(n_stages >= 1, "n_stages must be >= 1");
+    IL_REQUIRE(n_chains >= 1 && n_chains <= 8 && chains, "need 1..8 chains");
+    for (int c = 0; c < n_chains; ++c)
+        IL_REQUIRE(chains[c] == 0 || chains[c] == 1, "chain codes are 0 (mmse) and 1 (mmse_sic)");
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
+               "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
+    IL_REQUIRE(P == 0 || x_idx, "x_idx must not be NULL");
+    Alphabet al;
+    rc = make_qam_alphabet(qam_order, &al);
+    if (rc) return rc;
+    if (P == 0) return IL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = 2 * n_t, nx = 2 * n_t;
+    Workspace ws(st);
+    uint8_t* bx = ws.get<uint8_t>((size_t)n_chains * P * nx, &rc);    // baselines
+    double* be = ws.get<double>((size_t)n_chains * P, &rc);
+    int8_t* bst = ws.get<int8_t>((size_t)n_chains * P, &rc);
+    int32_t* codes = ws.get<int32_t>((size_t)n_chains, &rc);
+    uint8_t* gx = ws.get<uint8_t>((size_t)P * nx, &rc);                // chain guess
+    double* ge = ws.get<double>((size_t)P, &rc);
+    int8_t* ssrc = ws.get<int8_t>((size_t)P, &rc);
+    int32_t* sai = ws.get<int32_t>((size_t)P, &rc);
+    int32_t* sdc = ws.get<int32_t>((size_t)P, &rc);
+    int32_t* widx = ws.get<int32_t>((size_t)P, &rc);
+    double* en = energy ? energy : ws.get<double>((size_t)P, &rc);
+    int8_t* src = source ? source : ws.get<int8_t>((size_t)P, &rc);
+    int32_t* ai = anneal_index ? anneal_index : ws.get<int32_t>((size_t)P, &rc);
+    double* G = ws.get<double>((size_t)P * N * N, &rc);
+    double* g = ws.get<double>((size_t)P * N, &rc);
+    double* b = ws.get<double>((size_t)P * N, &rc);
+    double* off = ws.get<double>((size_t)P, &rc);
+    double* eps = ws.get<double>((size_t)P, &rc);
+    uint64_t* base = ws.get<uint64_t>((size_t)P, &rc);
+    if (rc) return rc;
+    IL_CHECK_CUDA(cudaMemcpyAsync(codes, chains, sizeof(int32_t) * n_chains,
+                                  cudaMemcpyHostToDevice, st));
+    for (int c = 0; c < n_chains; ++c) {  // baselines (detector.py:110-111)
+        uint8_t* x = bx + (size_t)c * P * nx;
+        rc = chains[c] == 0
+                 ? launch_mmse(H, y, noise_var, P, n_r, n_t, al, x, be + (size_t)c * P,
+                               bst + (size_t)c * P, st)
+                 : launch_mmse_sic(H, y, noise_var, P, n_r, n_t, al, x, be + (size_t)c * P,
+                                   bst + (size_t)c * P, st);
+        if (rc) return rc;
+    }
+    rc = launch_multi_init(bx, be, bst, codes, n_chains, P, nx, x_idx, en, src, ai, st);
+    if (rc) return rc;
+    if (diverged_count) IL_CHECK_CUDA(cudaMemsetAsync(diverged_count, 0, sizeof(int32_t) * P, st));
+    const double fixed = prm->eps > 0.0 ? prm->eps : 0.0;
+    for (int c = 0; c < n_chains; ++c) {  // chains x stages (detector.py:114-131)
+        IL_CHECK_CUDA(cudaMemcpyAsync(gx, bx + (size_t)c * P * nx, (size_t)P * nx,
+                                      cudaMemcpyDeviceToDevice, st));
+        IL_CHECK_CUDA(cudaMemcpyAsync(ge, be + (size_t)c * P, sizeof(double) * P,
+                                      cudaMemcpyDeviceToDevice, st));
+        IL_CHECK_CUDA(cudaMemsetAsync(widx, 0xff, sizeof(int32_t) * P, st));  // -1
+        for (int stage = 0; stage < n_stages; ++stage) {
+            rc = launch_build_ising(H, y, gx, P, n_r, n_t, al, G, g, b, off, nullptr, eps, 1.0,
+                                    fixed, st);
+            if (rc) return rc;
+            rc = launch_base_seeds(seed, P, (uint64_t)c, (uint64_t)stage, base, st);
+            if (rc) return rc;
+            IL_CHECK_CUDA(cudaMemsetAsync(ssrc, 0, (size_t)P, st));
+            rc = anneal_and_select(H, y, P, n_r, n_t, al, G, g, b, off, eps, base, prm, gx, ge,
+                                   ssrc, sai, sdc, ws, st);
+            if (rc) return rc;
+            rc = launch_multi_stage(sai, P, widx, st);
+            if (rc) return rc;
+            if (diverged_count) {
+                rc = launch_add_i32(sdc, P, diverged_count, st);
+                if (rc) return rc;
+            }
+        }
+        rc = launch_multi_combine(gx, ge, widx, P, nx, x_idx, en, src, ai, st);
+        if (rc) return rc;
+    }
+    return IL_OK;
+}
+
 int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_u, int32_t n_ant,
                          double power, double tau, int32_t n_stages, const uint64_t* seed,
                          const il_cac_params* prm, double* x, double* v, double* unnorm_power,

@@ -618,12 +618,37 @@ __global__ void k_base_seeds(const uint64_t* __restrict__ seed, int64_t P, uint6
     if (i < P) out[i] = derive_seed3(seed[i], k1, k2);
 }
 
+// ||y - Hx||^2 per problem for arbitrary complex x (linear.py:44-47), in the
+// library's one residual arithmetic (resid_row + 32-lane warp_sum).
+__global__ void k_residual(const double* __restrict__ Hg, const double* __restrict__ yg,
+                           const double* __restrict__ xg, int64_t P, int n_r, int n_t,
+                           double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (prob >= P) return;
+    const cplx* H = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n_t;
+    const cplx* y = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
+    const cplx* x = reinterpret_cast<const cplx*>(xg) + prob * (int64_t)n_t;
+    double acc = 0.0;
+    for (int k = lane; k < n_r; k += 32) acc = __dadd_rn(acc, abs2_rn(resid_row(H + k * n_t, x, n_t, y[k])));
+    acc = warp_sum(acc);
+    if (lane == 0) out[prob] = acc;
+}
+
 __global__ void k_add_i32(const int32_t* __restrict__ a, int64_t n, int32_t* __restrict__ acc) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) acc[i] += a[i];
 }
 
 }  // namespace
+
+int launch_residual(const double* H, const double* y, const double* x, int64_t P, int n_r, int n_t,
+                    double* out, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    IL_LAUNCH(kProfOther, st, k_residual<<<(unsigned)((P + 3) / 4), 128, 0, st>>>(H, y, x, P, n_r, n_t, out););
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
 
 int launch_add_i32(const int32_t* a, int64_t n, int32_t* acc, cudaStream_t st) {
     if (n == 0) return IL_OK;

@@ -74,9 +74,22 @@ int launch_mmse_ising(const double* H, const double* y, const double* noise_var,
                       int n_r, int n_t, const Alphabet& al, uint8_t* x_idx, double* energy,
                       int8_t* status, double* G, double* g_diag, double* b, double* offset,
                       double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st);
+// MMGaP-E (multi.cu)
+int launch_mmse_sic(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
+                    int n_t, const Alphabet& al, uint8_t* x_idx, double* energy, int8_t* status,
+                    cudaStream_t st);
+int launch_multi_init(const uint8_t* bx, const double* be, const int8_t* bst,
+                      const int32_t* codes, int n_chains, int64_t P, int nx, uint8_t* x,
+                      double* e, int8_t* src, int32_t* aidx, cudaStream_t st);
+int launch_multi_stage(const int32_t* stage_ai, int64_t P, int32_t* widx, cudaStream_t st);
+int launch_multi_combine(const uint8_t* gx, const double* ge, const int32_t* widx, int64_t P,
+                         int nx, uint8_t* x, double* e, int8_t* src, int32_t* aidx,
+                         cudaStream_t st);
 int launch_vpp_post(const double* W, const double* u, const double* y_t, const double* base_energy,
                     const uint8_t* vidx, int64_t P, int n_u, int n_ant, int reach, double tau,
                     double power, double* x, double* v, double* unnorm_power, cudaStream_t st);
+int launch_residual(const double* H, const double* y, const double* x, int64_t P, int n_r, int n_t,
+                    double* out, cudaStream_t st);
 int launch_add_i32(const int32_t* a, int64_t n, int32_t* acc, cudaStream_t st);
 int launch_gray_demap(const uint8_t* x_idx, int64_t n_sym, int bits_per_dim, uint8_t* bits,
                       cudaStream_t st);
