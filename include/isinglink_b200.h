@@ -142,6 +142,21 @@ int il_solve_batch(const double* G, const double* g_diag, const double* b,
                    int32_t* best_index, int32_t* diverged_count, int64_t* steps,
                    int64_t* mvms, void* stream);
 
+/* P x integrate_anneal (solver.py:217-235): one FP64-exact anneal per
+ * problem from default_rng(seed[p]).uniform(-amp, amp), coupling eps[p];
+ * spins[P*(2N+1)], diverged[P], steps[P], mvms[P], energy[P] (may be NULL).
+ * Drives the Appendix-A integration heatmap (harness/heatmap.py). */
+int il_integrate_batch(const double* G, const double* g_diag, const double* b,
+                       const double* eps, const uint64_t* seed, int64_t P, int32_t n_dim,
+                       const il_cac_params* prm, int8_t* spins, uint8_t* diverged,
+                       int64_t* steps, int64_t* mvms, double* energy, void* stream);
+
+/* Exhaustive ML detection (linear.py:109-144), ties to the smallest symbol-
+ * index vector (user 0 most significant); refuses > 24-bit search spaces.
+ * x_idx[P*n_t*2] level indices, energy[P] residual (may be NULL). */
+int il_ml_batch(const double* H, const double* y, int64_t P, int32_t n_r, int32_t n_t,
+                int32_t qam_order, uint8_t* x_idx, double* energy, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Batched uplink detection: P x detect_cim (detector.py:57-82) with
  * seed[p] the `seed` argument of detect_cim for problem p.  Outputs:

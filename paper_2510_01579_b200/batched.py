@@ -196,6 +196,42 @@ def residual_batch(H, y, x) -> torch.Tensor:
     return out
 
 
+def ml_batch(H, y, order: int):
+    """P x ``detect_ml`` (linear.py:109-144) -> (x_idx, energy)."""
+    Hd = _dev(H, torch.complex128)
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    x_idx = torch.empty((P, n_t, 2), dtype=torch.uint8, device=Hd.device)
+    energy = torch.empty(P, dtype=torch.float64, device=Hd.device)
+    _lib.call("il_ml_batch", Hd.data_ptr(), yd.data_ptr(), P, n_r, n_t, int(order),
+              x_idx.data_ptr(), energy.data_ptr(), _stream())
+    return x_idx, energy
+
+
+def integrate_batch(G, g_diag, b, eps, seeds, params=None) -> dict:
+    """P x ``integrate_anneal`` (solver.py:217-235), FP64-exact: problem p
+    starts from default_rng(seeds[p]) with coupling eps[p]."""
+    params = params or CacParams()
+    prm = to_c(params, "fp64_exact")
+    Gd = _dev(G, torch.float64)
+    P, N, _ = Gd.shape
+    gd = _dev(g_diag, torch.float64)
+    bd = _dev(b, torch.float64)
+    ed = _dev(eps, torch.float64).reshape(P)
+    sd = _seeds(seeds, P)
+    dev = Gd.device
+    out = dict(spins=torch.empty((P, 2 * N + 1), dtype=torch.int8, device=dev),
+               diverged=torch.empty(P, dtype=torch.uint8, device=dev),
+               steps=torch.empty(P, dtype=torch.int64, device=dev),
+               mvms=torch.empty(P, dtype=torch.int64, device=dev),
+               energy=torch.empty(P, dtype=torch.float64, device=dev))
+    _lib.call("il_integrate_batch", Gd.data_ptr(), gd.data_ptr(), bd.data_ptr(), ed.data_ptr(),
+              sd.data_ptr(), P, N, prm, out["spins"].data_ptr(), out["diverged"].data_ptr(),
+              out["steps"].data_ptr(), out["mvms"].data_ptr(), out["energy"].data_ptr(),
+              _stream())
+    return out
+
+
 def mmse_sic_batch(H, y, noise_var, order: int):
     """P x ``detect_mmse_sic`` (linear.py:78-106) -> (x_idx, energy, status)."""
     Hd = _dev(H, torch.complex128)

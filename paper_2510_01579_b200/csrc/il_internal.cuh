@@ -85,6 +85,10 @@ int launch_multi_stage(const int32_t* stage_ai, int64_t P, int32_t* widx, cudaSt
 int launch_multi_combine(const uint8_t* gx, const double* ge, const int32_t* widx, int64_t P,
                          int nx, uint8_t* x, double* e, int8_t* src, int32_t* aidx,
                          cudaStream_t st);
+int launch_ml(const double* H, const double* y, int64_t P, int n_r, int n_t, const Alphabet& al,
+              uint8_t* x_idx, double* energy, cudaStream_t st);
+int launch_spin_energies(const double* G, const double* b, const int8_t* spins, int64_t P, int B,
+                         int N, double* out, cudaStream_t st);
 int launch_vpp_post(const double* W, const double* u, const double* y_t, const double* base_energy,
                     const uint8_t* vidx, int64_t P, int n_u, int n_ant, int reach, double tau,
                     double power, double* x, double* v, double* unnorm_power, cudaStream_t st);

@@ -163,4 +163,39 @@ int il_solve_batch(const double* G, const double* g_diag, const double* b, const
     return IL_OK;
 }
 
+int il_integrate_batch(const double* G, const double* g_diag, const double* b, const double* eps,
+                       const uint64_t* seed, int64_t P, int32_t n_dim, const il_cac_params* prm,
+                       int8_t* spins, uint8_t* diverged, int64_t* steps, int64_t* mvms,
+                       double* energy, void* stream) {
+    IL_REQUIRE(prm != nullptr, "params must not be NULL");
+    IL_REQUIRE(P >= 0 && n_dim >= 1 && n_dim <= 128, "invalid shape");
+    IL_REQUIRE(prm->dt > 0 && prm->f_mvm >= 1 && prm->n_steps >= 1, "invalid solver parameters");
+    IL_REQUIRE(P == 0 || (spins && diverged && steps && mvms && seed && eps), "NULL buffer");
+    if (P == 0) return IL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int N = n_dim, S = 2 * N + 1;
+    AnnealScalars s{};
+    s.p = prm->p;
+    s.a = prm->a;
+    s.zeta = prm->zeta;
+    s.dt = prm->dt;
+    s.e_floor = prm->e_floor;
+    s.thr = prm->diverge_threshold;
+    s.x0_lo = -prm->init_amplitude;
+    s.x0_range = prm->init_amplitude - (-prm->init_amplitude);
+    s.f_mvm = prm->f_mvm;
+    s.n_steps = prm->n_steps;
+    int rc = IL_OK;
+    Workspace ws(st);
+    double* x0 = ws.get<double>((size_t)P * S, &rc);
+    if (rc) return rc;
+    // integrate_anneal draws x0 from default_rng(seed) itself (solver.py:227)
+    rc = il_initial_states(seed, P, S, prm->init_amplitude, x0, st);
+    if (rc) return rc;
+    rc = launch_anneal_exact(G, g_diag, b, x0, nullptr, eps, P, N, 1, s, spins, diverged, steps,
+                             mvms, st);
+    if (rc) return rc;
+    return energy ? launch_spin_energies(G, b, spins, P, 1, N, energy, st) : IL_OK;
+}
+
 }  // extern "C"

@@ -202,9 +202,45 @@ def main_multi():
     print("MMGaP-E / SIC / ML fixtures written to", HERE)
 
 
+HARNESS_CASES = [  # (file stem, config overrides) -> reference CSV + config text
+    ("sweep_up_4x4_qpsk", dict(mode="uplink_sweep", n_r=4, n_t=4, modulation=4,
+                               snr_grid_db=(5.0, 15.0), n_trials=48, n_stages=2, seed=7,
+                               detectors=("mmse", "mmse_sic", "ml", "cim", "cim_multi"))),
+    ("sweep_up_8x8_16qam", dict(mode="uplink_sweep", n_r=8, n_t=8, modulation=16,
+                                snr_grid_db=(15.0, 25.0), n_trials=32, seed=8,
+                                detectors=("mmse", "mmse_sic", "cim", "cim_multi"))),
+    ("sweep_down_4x4_16qam", dict(mode="downlink_sweep", n_r=4, n_t=4, modulation=16,
+                                  snr_grid_db=(10.0, 20.0), n_trials=24, seed=9)),
+    ("heatmap_8x8_16qam", dict(mode="heatmap", n_r=8, n_t=8, modulation=16,
+                               snr_grid_db=(10.0,), n_instances=32, seed=10)),
+]
+
+
+def main_harness():
+    """The reference's own sweep / heatmap CSVs (harness/sweeps.py, heatmap.py)."""
+    import dataclasses
+    import_reference()
+    from isinglink.harness.config import ExperimentConfig, format_config
+    from isinglink.harness.heatmap import run_integration_heatmap
+    from isinglink.harness.sweeps import run_detection_sweep, run_precoding_sweep
+    run = {"uplink_sweep": run_detection_sweep, "downlink_sweep": run_precoding_sweep,
+           "heatmap": run_integration_heatmap}
+    for stem, over in HARNESS_CASES:
+        cfg = dataclasses.replace(ExperimentConfig(), output_path=os.path.join(HERE, stem + ".csv"),
+                                  **over)
+        run[cfg.mode](cfg)
+        with open(os.path.join(HERE, stem + ".cfg"), "w") as fh:
+            fh.write(format_config(dataclasses.replace(cfg, output_path="")))
+    print("harness fixtures written to", HERE)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "harness":
+        main_harness()
+        raise SystemExit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "multi":
         main_multi()
     else:
         main()
         main_multi()
+        main_harness()
