@@ -125,11 +125,12 @@ def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
         raise TypeError("seeds must be uint64 (or int64 bit patterns)")
     st = _host(st, st.dtype, (P,))
     if out is None:
-        out = DetectBatch(x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8),
-                          energy=torch.empty(P, dtype=torch.float64),
-                          source=torch.empty(P, dtype=torch.int8),
-                          anneal_index=torch.empty(P, dtype=torch.int32),
-                          diverged=torch.empty(P, dtype=torch.int32))
+        pin = torch.cuda.is_available()
+        out = DetectBatch(x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8, pin_memory=pin),
+                          energy=torch.empty(P, dtype=torch.float64, pin_memory=pin),
+                          source=torch.empty(P, dtype=torch.int8, pin_memory=pin),
+                          anneal_index=torch.empty(P, dtype=torch.int32, pin_memory=pin),
+                          diverged=torch.empty(P, dtype=torch.int32, pin_memory=pin))
     _lib.call("il_detect_cim_host", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(), P, n_r, n_t,
               int(order), st.data_ptr(), prm, out.x_idx.data_ptr(), out.energy.data_ptr(),
               out.source.data_ptr(), out.anneal_index.data_ptr(), out.diverged.data_ptr(),

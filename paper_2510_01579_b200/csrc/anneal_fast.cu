@@ -52,6 +52,15 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_LOOP2  // refresh-period outer loop, f_mvm Euler steps inner
 #define IL_LOOP2 0
 #endif
+#ifndef IL_FUSE1  // as IL_LOOP2, first Euler step fused into the refresh block
+#define IL_FUSE1 0
+#endif
+#ifndef IL_NOUTER  // MMA issue order: n-tile outer (early accumulators)
+#define IL_NOUTER 0
+#endif
+#ifndef IL_PB2  // packed partial sums for the aux coupling
+#define IL_PB2 0
+#endif
 
 struct FastScalars {
     float alpha;    // 1 + dt (p - 1)
@@ -245,7 +254,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     }
     __syncwarp();
 
-#if IL_LOOP2
+#if IL_LOOP2 || IL_FUSE1
     for (int step0 = 0; step0 < s.n_steps; step0 += s.f_mvm) {
         {
 #else
@@ -257,6 +266,21 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             // ---- refresh: v = x1 + x2, M' = -Ks G v on tensor cores -----------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
+#if IL_PB2
+            // packed partial sums of -Ks b.v over the thread's spin pairs; every
+            // lane of a quad sums the same pairs in the same order, so the two
+            // owner lanes of an aux spin still agree bit for bit
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float2 p2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    v[h][n] = __fadd2_rn(xA[h][n], xB[h][n]);
+                    p2 = __ffma2_rn(nKb[n], v[h][n], p2);
+                }
+                pb[h] = p2.x + p2.y;
+            }
+#else
 #pragma unroll
             for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -265,6 +289,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                     pb[h] = fmaf(nKb[n].x, v[h][n].x, pb[h]);
                     pb[h] = fmaf(nKb[n].y, v[h][n].y, pb[h]);
                 }
+#endif
             // aux states of both anneals of the quad, from their owner lanes
             const float xa0 = __shfl_sync(0xffffffffu, xa, (lane & ~3) | 0);
             const float xa1 = __shfl_sync(0xffffffffu, xa, (lane & ~3) | 1);
@@ -286,6 +311,35 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
             for (int n = 0; n < NT; ++n) acc2[n][0] = acc2[n][1] = acc2[n][2] = acc2[n][3] = 0.f;
 #endif
+#if IL_NOUTER
+            // all A fragments first, then one n-tile at a time: acc[n] completes
+            // early, so its coupling assembly (and the Euler step, in the same
+            // block) can overlap the tensor work of the next tiles
+            uint32_t AH[KT][4], AL[KT][4];
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                split_h2(v[0][2 * kt], AH[kt][0], AL[kt][0]);
+                split_h2(v[1][2 * kt], AH[kt][1], AL[kt][1]);
+                if (2 * kt + 1 < NT) {
+                    split_h2(v[0][2 * kt + 1], AH[kt][2], AL[kt][2]);
+                    split_h2(v[1][2 * kt + 1], AH[kt][3], AL[kt][3]);
+                } else {
+                    AH[kt][2] = AH[kt][3] = AL[kt][2] = AL[kt][3] = 0u;
+                }
+            }
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) {
+                    const uint4 f = frag[(kt * NT + n) * 32 + lane];
+                    if (SPLIT) {
+                        mma_f16(acc[n], AL[kt], f.x, f.y);
+                        mma_f16(acc[n], AH[kt], f.z, f.w);
+                    }
+                    mma_f16(acc[n], AH[kt], f.x, f.y);
+                }
+            }
+#else
 #pragma unroll
             for (int kt = 0; kt < KT; ++kt) {
                 // A fragment: a0 = (g, 2t..), a1 = (g+8, 2t..), a2 = (g, 2t+8..), a3 = (g+8, 2t+8..)
@@ -313,6 +367,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                     mma_f16(acc[n], ahi, f.x, f.y);
                 }
             }
+#endif
             // ---- coupling assembly: C_s = M' + Ks g x_self - Ks b xa ----------
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -332,7 +387,20 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 }
             }
         }
-#if IL_LOOP2
+#if IL_FUSE1
+        // first Euler step of the period in the refresh's basic block
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, e_floor, dv[h][n & 1]);
+                euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
+            }
+        }
+        euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
+        const int n_in = min(s.f_mvm, s.n_steps - step0);
+        for (int k = 1; k < n_in; ++k) {
+#elif IL_LOOP2
         const int n_in = min(s.f_mvm, s.n_steps - step0);
 #pragma unroll 2
         for (int k = 0; k < n_in; ++k) {
@@ -346,7 +414,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             }
         }
         euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
-#if IL_LOOP2
+#if IL_LOOP2 || IL_FUSE1
         }
 #else
         --until_refresh;

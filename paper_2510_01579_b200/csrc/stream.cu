@@ -8,7 +8,7 @@
 // alternate between two compute streams so the next chunk's front-end can
 // fill SMs while the previous chunk's anneal drains.  Pinned host memory is
 // required for the overlap (pageable memory works but the copies then
-// serialise with the host thread).
+// serialise with the host thread; pageable outputs only delay the tail).
 #include <algorithm>
 #include <vector>
 
@@ -59,7 +59,7 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
     IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && x_idx), "NULL buffer");
     if (P == 0) return IL_OK;
     keep_pool_warm();
-    if (n_chunks <= 0) n_chunks = P >= 16384 ? 8 : (P >= 4096 ? 4 : 1);
+    if (n_chunks <= 0) n_chunks = P >= 32768 ? 12 : (P >= 16384 ? 8 : (P >= 4096 ? 4 : 1));
     n_chunks = (int)std::min<int64_t>(std::min(n_chunks, 64), P);
     int64_t chunk = (P + n_chunks - 1) / n_chunks;
     chunk = (chunk + 7) / 8 * 8;
@@ -114,6 +114,12 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
                                      ddc + o, cs);
             if (rc) break;
             cudaEventRecord(ss.ev[2 * c + 1], cs);
+        }
+        // D2H copies are enqueued after every chunk's H2D and compute: a copy
+        // into pageable memory blocks the host thread, which must not delay
+        // the enqueue of later chunks (the outputs are ~1% of the inputs)
+        for (int c = 0; c < n_chunks && rc == IL_OK; ++c) {
+            const int64_t o = c * chunk, n = std::min(chunk, P - o);
             cudaStreamWaitEvent(ss.out, ss.ev[2 * c + 1], 0);
             cudaMemcpyAsync(x_idx + o * xsz, dx + o * xsz, xsz * n, cudaMemcpyDeviceToHost, ss.out);
             if (energy)
