@@ -11,7 +11,8 @@ Entry points:
   * ``api``           — the reference's per-instance API (detect_cim, precode_vpp,
     build_ising, solve_batch, ...) running on the GPU;
   * ``batched``       — whole-slot device API (detect_cim_batch, precode_vpp_batch, ...);
-  * ``shard``         — subcarrier sharding over GPUs with an NCCL gather of bits.
+  * ``shard``         — subcarrier sharding over GPUs with an NCCL gather of bits;
+  * ``harness``       — the reference's sweeps / heatmap / bench report on the GPU.
 """
 
 from . import _lib
