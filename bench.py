@@ -250,10 +250,18 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: ISINGLINK_BENCH_DEVICE pins every rank to one device and
+    # ISINGLINK_BENCH_BACKEND=gloo replaces NCCL, so the multi-rank path can be
+    # exercised on a single-GPU box; the driver's runs use one GPU per rank
+    local = int(os.environ.get("ISINGLINK_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("ISINGLINK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     _lib.load()
     shard = slot_shard(N_PRB, rank, world)
     P_all = shard.n_res

@@ -61,6 +61,12 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_PB2  // packed partial sums for the aux coupling
 #define IL_PB2 0
 #endif
+#ifndef IL_LAZY_FLOOR  // one min per step decides whether the e floor binds
+#define IL_LAZY_FLOOR 0
+#endif
+#if IL_LAZY_FLOOR && IL_FUSE1
+#error "IL_LAZY_FLOOR is implemented for the default loop structure only"
+#endif
 
 struct FastScalars {
     float alpha;    // 1 + dt (p - 1)
@@ -124,7 +130,23 @@ __device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
     const float2 t = __fmul2_rn(x, q);
     x = __ffma2_rn(e, C, t);
     const float2 er = __fmul2_rn(e, r);
+#if IL_LAZY_FLOOR
+    // floor applied by the caller only if some e of the step fell below it
+    e = er;
+    (void)e_floor;
+#else
     e = make_float2(fmaxf(er.x, e_floor), fmaxf(er.y, e_floor));
+#endif
+}
+
+__device__ __forceinline__ float min_nan3(float a, float b, float c) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    asm("min.NaN.f32 %0, %0, %1;" : "+f"(r) : "f"(c));
+    return r;
+}
+__device__ __forceinline__ float2 floor2(float2 e, float f) {
+    return make_float2(fmaxf(e.x, f), fmaxf(e.y, f));
 }
 
 template <bool SAME_QR>
@@ -413,6 +435,31 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
             }
         }
+#if IL_LAZY_FLOOR
+        // e' = max(e_floor, e q): one NaN-propagating min over the step's new
+        // e values decides whether any floor binds (rare: e starts at 1 and
+        // shrinks only where x^2 > a); the result is identical to clamping
+        // every element, a NaN e takes the clamping path as before
+        {
+            float em = INFINITY;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    em = min_nan3(em, eA[h][n].x, eA[h][n].y);
+                    em = min_nan3(em, eB[h][n].x, eB[h][n].y);
+                }
+            if (!(em >= e_floor)) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int n = 0; n < NT; ++n) {
+                        eA[h][n] = floor2(eA[h][n], e_floor);
+                        eB[h][n] = floor2(eB[h][n], e_floor);
+                    }
+            }
+        }
+#endif
         euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
 #if IL_LOOP2 || IL_FUSE1
         }

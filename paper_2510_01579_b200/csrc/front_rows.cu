@@ -28,6 +28,10 @@ namespace il {
 namespace {
 
 constexpr int kRowsThreads = 128;
+#ifndef IL_GRAM_UNROLL
+#define IL_GRAM_UNROLL 1
+#endif
+constexpr int kGramUnroll = IL_GRAM_UNROLL;
 
 // Per-group shared-memory slice (cplx units).
 IL_HD size_t rows_group_cplx(int n_r, int n, int GS) {
@@ -47,6 +51,7 @@ __device__ __forceinline__ void gram_row(const cplx* H, const cplx* y, int n_r, 
     for (int j = 0; j < GS; ++j) A[j] = {0.0, 0.0}, im2[j] = 0.0;
     cplx zz = {0.0, 0.0};
     const bool own = r < n;
+#pragma unroll kGramUnroll
     for (int k = 0; k < n_r; ++k) {
         const cplx* Hk = H + k * n;
         const cplx hr = own ? Hk[r] : cplx{0.0, 0.0};
