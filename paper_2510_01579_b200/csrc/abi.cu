@@ -122,24 +122,30 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
                              int8_t* source, int32_t* anneal_index, int32_t* diverged_count,
                              Workspace& ws, cudaStream_t st) {
     const int N = 2 * n_t, S = 2 * N + 1, B = prm->n_anneals;
-    int rc = IL_OK;
-    int8_t* spins = ws.get<int8_t>((size_t)P * B * S, &rc);
-    uint8_t* div = ws.get<uint8_t>((size_t)P * B, &rc);
-    if (rc) return rc;
     const AnnealScalars s = scalars_of(prm);
+    // the fast kernel runs anneals in tiles of 16: B is padded (anneal r of a
+    // problem is seeded by r alone, so the extra rows change nothing) and the
+    // selection reads the first B rows of each problem
+    const bool fast = prm->precision != IL_PREC_FP64_EXACT &&
+                      fast_anneal_supported(N, fast_rows(B), s);
+    const int Bs = fast ? fast_rows(B) : B;
+    int rc = IL_OK;
+    int8_t* spins = ws.get<int8_t>((size_t)P * Bs * S, &rc);
+    uint8_t* div = ws.get<uint8_t>((size_t)P * Bs, &rc);
+    if (rc) return rc;
     double* energies = nullptr;
-    if (prm->precision != IL_PREC_FP64_EXACT && fast_anneal_supported(N, B, s)) {
-        energies = ws.get<double>((size_t)P * B, &rc);
+    if (fast) {
+        energies = ws.get<double>((size_t)P * Bs, &rc);
         if (rc) return rc;
-        rc = launch_anneal_fast(G, g, b, base, eps, P, N, B, s, prm->precision, spins, div,
+        rc = launch_anneal_fast(G, g, b, base, eps, P, N, Bs, s, prm->precision, spins, div,
                                 energies, st);
     } else {
         rc = launch_anneal_exact(G, g, b, nullptr, base, eps, P, N, B, s, spins, div, nullptr,
                                  nullptr, st);
     }
     if (rc) return rc;
-    return launch_select_decode(H, y, G, b, offset, spins, div, energies, P, n_r, n_t, B, al, x_idx,
-                                energy, source, anneal_index, diverged_count, st);
+    return launch_select_decode(H, y, G, b, offset, spins, div, energies, P, n_r, n_t, B, Bs, al,
+                                x_idx, energy, source, anneal_index, diverged_count, st);
 }
 
 }  // namespace il

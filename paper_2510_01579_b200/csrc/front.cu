@@ -366,7 +366,7 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
                                 const double* __restrict__ offset, const int8_t* __restrict__ spins,
                                 const uint8_t* __restrict__ diverged,
                                 const double* __restrict__ energies, int64_t P, int n_r, int n_t,
-                                int B, Alphabet al, uint8_t* __restrict__ x_idx,
+                                int B, int Bs, Alphabet al, uint8_t* __restrict__ x_idx,
                                 double* __restrict__ energy, int8_t* __restrict__ source,
                                 int32_t* __restrict__ anneal_index,
                                 int32_t* __restrict__ diverged_count) {
@@ -401,15 +401,17 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
     // energies: lane = anneal, E = u'Gu - 2 tr G + 2 s_aux b'u  (solver.py:171-175)
     double best_e = INFINITY;
     int best_i = -1, ndiv = 0;
-    const int8_t* sp0 = spins + prob * (int64_t)B * S;
+    // B anneals per problem in rows of stride Bs >= B (the fast kernel pads
+    // B to a multiple of 16; padded anneals never enter the selection)
+    const int8_t* sp0 = spins + prob * (int64_t)Bs * S;
     for (int a0 = 0; a0 < B; a0 += 32) {
         const int a = a0 + lane;
         double ea = INFINITY;
         if (a < B) {
-            const bool dv = diverged[prob * B + a] != 0;
+            const bool dv = diverged[prob * Bs + a] != 0;
             ndiv += dv;
             if (!dv && energies) {
-                ea = energies[prob * B + a];
+                ea = energies[prob * Bs + a];
             } else if (!dv) {
                 const int8_t* s = sp0 + (int64_t)a * S;
                 double quad = 0.0, lin = 0.0;
@@ -728,7 +730,7 @@ int launch_mmse_ising(const double* H, const double* y, const double* noise_var,
 
 int launch_select_decode(const double* H, const double* y, const double* G, const double* b,
                          const double* offset, const int8_t* spins, const uint8_t* diverged,
-                         const double* energies, int64_t P, int n_r, int n_t, int B,
+                         const double* energies, int64_t P, int n_r, int n_t, int B, int Bs,
                          const Alphabet& al, uint8_t* x_idx_io, double* energy_io,
                          int8_t* source, int32_t* anneal_index, int32_t* diverged_count,
                          cudaStream_t st) {
@@ -744,7 +746,7 @@ int launch_select_decode(const double* H, const double* y, const double* G, cons
     if (rc) return rc;
     const int blocks = (int)((P + wpb - 1) / wpb);
     IL_LAUNCH(kProfSelect, st, k_select_decode<<<blocks, 32 * wpb, smem, st>>>(H, y, G, b, offset, spins, diverged, energies, P, n_r,
-                                                    n_t, B, al, x_idx_io, energy_io, source,
+                                                    n_t, B, Bs, al, x_idx_io, energy_io, source,
                                                     anneal_index, diverged_count););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;

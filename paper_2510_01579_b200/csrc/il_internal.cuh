@@ -29,6 +29,8 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
                        double* energies, cudaStream_t st);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
+// anneal rows per problem the fast kernel runs for B requested anneals
+inline int fast_rows(int B) { return (B + 15) / 16 * 16; }
 
 // ---- front-end / reduction kernels -----------------------------------------
 // Ising outputs of the front-end kernels (any pointer may be null).
@@ -65,7 +67,7 @@ int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, in
 // x_idx_io holds the guess on entry and the result on exit.
 int launch_select_decode(const double* H, const double* y, const double* G, const double* b,
                          const double* offset, const int8_t* spins, const uint8_t* diverged,
-                         const double* energies, int64_t P, int n_r, int n_t, int B,
+                         const double* energies, int64_t P, int n_r, int n_t, int B, int Bs,
                          const Alphabet& al,
                          uint8_t* x_idx_io, double* energy_io, int8_t* source,
                          int32_t* anneal_index, int32_t* diverged_count, cudaStream_t st);

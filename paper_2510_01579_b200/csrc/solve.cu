@@ -41,7 +41,7 @@ __global__ void k_spin_energies(const double* __restrict__ Gg, const double* __r
 // and the winner's spins.  One warp per problem.
 __global__ void k_select_best(const double* __restrict__ energies, const uint8_t* __restrict__ div,
                               const int8_t* __restrict__ spins, const double* __restrict__ offset,
-                              const double* __restrict__ fallback, int64_t P, int B, int S,
+                              const double* __restrict__ fallback, int64_t P, int B, int Bs, int S,
                               int8_t* __restrict__ best_spins, double* __restrict__ best_energy,
                               int32_t* __restrict__ best_index, int32_t* __restrict__ ndiv_out) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -50,9 +50,9 @@ __global__ void k_select_best(const double* __restrict__ energies, const uint8_t
     double be = INFINITY;
     int bi = -1, nd = 0;
     for (int a = lane; a < B; a += 32) {
-        const bool d = div[prob * B + a] != 0;
+        const bool d = div[prob * Bs + a] != 0;
         nd += d;
-        const double e = d ? INFINITY : energies[prob * B + a];
+        const double e = d ? INFINITY : energies[prob * Bs + a];
         if (e < be) {
             be = e;
             bi = a;
@@ -76,7 +76,7 @@ __global__ void k_select_best(const double* __restrict__ energies, const uint8_t
         if (best_index) best_index[prob] = keep ? bi : -1;
     }
     if (best_spins && bi >= 0) {
-        const int8_t* s = spins + (prob * B + bi) * (int64_t)S;
+        const int8_t* s = spins + (prob * Bs + bi) * (int64_t)S;
         for (int i = lane; i < S; i += 32) best_spins[prob * S + i] = s[i];
     }
 }
@@ -138,14 +138,17 @@ int il_solve_batch(const double* G, const double* g_diag, const double* b, const
     s.n_steps = prm->n_steps;
     int rc = IL_OK;
     Workspace ws(st);
-    int8_t* spins = ws.get<int8_t>((size_t)P * B * S, &rc);
-    uint8_t* div = ws.get<uint8_t>((size_t)P * B, &rc);
-    double* en = ws.get<double>((size_t)P * B, &rc);
-    if (rc) return rc;
     const bool want_counts = steps != nullptr || mvms != nullptr;
-    if (!want_counts && prm->precision != IL_PREC_FP64_EXACT && fast_anneal_supported(N, B, s)) {
-        rc = launch_anneal_fast(G, g_diag, b, base_seed, eps, P, N, B, s, prm->precision, spins, div,
-                                en, st);
+    const bool fast = !want_counts && prm->precision != IL_PREC_FP64_EXACT &&
+                      fast_anneal_supported(N, fast_rows(B), s);
+    const int Bs = fast ? fast_rows(B) : B;  // padded rows are never selected
+    int8_t* spins = ws.get<int8_t>((size_t)P * Bs * S, &rc);
+    uint8_t* div = ws.get<uint8_t>((size_t)P * Bs, &rc);
+    double* en = ws.get<double>((size_t)P * Bs, &rc);
+    if (rc) return rc;
+    if (fast) {
+        rc = launch_anneal_fast(G, g_diag, b, base_seed, eps, P, N, Bs, s, prm->precision, spins,
+                                div, en, st);
         if (rc) return rc;
     } else {
         rc = launch_anneal_exact(G, g_diag, b, nullptr, base_seed, eps, P, N, B, s, spins, div, steps,
@@ -157,7 +160,7 @@ int il_solve_batch(const double* G, const double* g_diag, const double* b, const
     const int wpb = 4;
     IL_LAUNCH(kProfSelect, st,
               k_select_best<<<(unsigned)((P + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
-                  en, div, spins, offset, fallback_energy, P, B, S, best_spins, best_energy,
+                  en, div, spins, offset, fallback_energy, P, B, Bs, S, best_spins, best_energy,
                   best_index, diverged_count));
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;

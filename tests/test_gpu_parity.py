@@ -224,3 +224,29 @@ def test_detect_cim_host_rejects_device_buffers():
     with pytest.raises(ValueError):
         batched.detect_cim_host(H, torch.zeros((2, 4), dtype=torch.complex128),
                                 torch.ones(2, dtype=torch.float64), 4, np.arange(2, dtype=np.uint64))
+
+
+@pytest.mark.parametrize("n_anneals", [8, 12, 40])
+def test_fast_kernel_any_replica_count(n_anneals):
+    """Replica counts that are not multiples of 16 (config 5's N_a sweep) run
+    on the fast kernel with padded tiles; the padded anneals never win."""
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    d = load_golden("d16x16_16qam_20db.npz")
+    args = (d["H"], d["y"], d["noise_var"], int(d["order"]), d["seed"])
+    ex = batched.detect_cim_batch(*args, CacParams(n_anneals=n_anneals, precision="fp64_exact"))
+    fa = batched.detect_cim_batch(*args, CacParams(n_anneals=n_anneals, precision="fp32"))
+    assert int(fa.anneal_index.max()) < n_anneals
+    assert int(fa.diverged.max()) <= n_anneals
+    e_ex, e_fa = ex.energy.cpu().numpy(), fa.energy.cpu().numpy()
+    assert (e_fa <= e_ex * (1 + 1e-12)).mean() >= 0.99
+    same = np.all(fa.x_idx.cpu().numpy() == ex.x_idx.cpu().numpy(), axis=(1, 2)).mean()
+    assert same >= 0.98
+    # the exact mode with B anneals is the oracle's detect_cim with n_anneals=B
+    levels, _ = orc.qam(int(d["order"]))
+    prm = orc.params(n_anneals=n_anneals)
+    for i in range(8):
+        r = orc.detect_cim(d["H"][i], d["y"][i], float(d["noise_var"][i]), int(d["order"]), prm,
+                           seed=int(d["seed"][i]))
+        want = np.stack([orc.level_index(r["x"].real, levels), orc.level_index(r["x"].imag, levels)], -1)
+        assert np.array_equal(ex.x_idx[i].cpu().numpy(), want)
