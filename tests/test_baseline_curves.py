@@ -1,0 +1,134 @@
+"""GPU: reproduce the reference's SER/BER curves of BASELINE.md §4 (CPU
+reference, paired instances, seed 1) through the GPU harness.
+
+With the reference's replayed initial states the FP64-exact mode must give
+the same SER/BER to the printed precision (half a unit of the last printed
+digit); the FP32 throughput mode must land inside the reference's binomial
+95% confidence interval (north_star BER-parity gate)."""
+
+import dataclasses
+import math
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SNR = (0.0, 5.0, 10.0, 15.0, 20.0, 25.0)
+# config -> (cfg overrides, {detector: [(ser_str, ber_str) per SNR]}) from BASELINE.md §4
+TABLES = {
+    "cfg1_8x8_qpsk": (dict(n_r=8, n_t=8, modulation=4, snr_grid_db=SNR, n_trials=896), {
+        "mmse": [("0.3898", "0.2191"), ("0.2306", "0.1232"), ("0.1049", "0.0543"),
+                 ("0.0364", "0.0187"), ("0.0105", "0.00544"), ("0.00293", "0.00153")],
+        "mmse_sic": [("0.4023", "0.2258"), ("0.2303", "0.1243"), ("0.0509", "0.0270"),
+                     ("0.00419", "0.00237"), ("0", "0"), ("0", "0")],
+        "cim": [("0.3976", "0.2249"), ("0.2373", "0.1287"), ("0.0539", "0.0289"),
+                ("0.00530", "0.00314"), ("0.000140", "0.0000698"), ("0", "0")],
+    }),
+    "cfg2_8x8_16qam": (dict(n_r=8, n_t=8, modulation=16, snr_grid_db=(10.0, 15.0, 20.0, 25.0, 30.0),
+                            n_trials=2000), {
+        "mmse": [("0.5918", "0.1883"), ("0.3827", "0.1128"), ("0.2088", "0.0592"),
+                 ("0.0811", "0.0224"), ("0.0283", "0.00784")],
+        "cim": [("0.5848", "0.1925"), ("0.3301", "0.1008"), ("0.0898", "0.0285"),
+                ("0.0193", "0.00631"), ("0.00688", "0.00228")],
+        "mmse_sic": [("0.5958", "0.1954"), ("0.3259", "0.1011"), ("0.0608", "0.0189"),
+                     ("0.00275", "0.000891"), ("0.00100", "0.000531")],
+        "cim_multi": [("0.5691", "0.1862"), ("0.2563", "0.0790"), ("0.0228", "0.00713"),
+                      ("0.00213", "0.000703"), ("0.000938", "0.000422")],
+    }),
+    "cfg3_16x16_16qam": (dict(n_r=16, n_t=16, modulation=16,
+                              snr_grid_db=(10.0, 15.0, 20.0, 25.0, 30.0), n_trials=1000), {
+        "mmse": [("0.5941", "0.1885"), ("0.4183", "0.1222"), ("0.2245", "0.0621"),
+                 ("0.1013", "0.0270"), ("0.0331", "0.00877")],
+        "cim": [("0.6006", "0.1949"), ("0.4331", "0.1299"), ("0.1986", "0.0582"),
+                ("0.0651", "0.0189"), ("0.0191", "0.00575")],
+    }),
+    "cfg5_16x16_64qam": (dict(n_r=16, n_t=16, modulation=64,
+                              snr_grid_db=(15.0, 20.0, 25.0, 30.0, 35.0), n_trials=1000), {
+        "mmse": [("0.7890", "0.2135"), ("0.6542", "0.1545"), ("0.4491", "0.0948"),
+                 ("0.2414", "0.0475"), ("0.0912", "0.0172")],
+        "cim": [("0.7836", "0.2127"), ("0.6639", "0.1587"), ("0.4613", "0.0999"),
+                ("0.2310", "0.0478"), ("0.0777", "0.0155")],
+    }),
+}
+DOWNLINK = (dict(mode="downlink_sweep", n_r=8, n_t=8, modulation=16,
+                 snr_grid_db=(10.0, 15.0, 20.0, 25.0, 30.0), n_trials=1000), {
+    "zf": [("0.4470", "0.1591"), ("0.1928", "0.0663"), ("0.0749", "0.0238"),
+           ("0.0235", "0.00759"), ("0.0095", "0.00319")],
+    "vpp": [("0.4086", "0.1310"), ("0.1409", "0.0410"), ("0.0226", "0.00594"),
+            ("0.00325", "0.000938"), ("0.00225", "0.000969")],
+})
+# replica sweep at 30 dB, 800 trials: N_a -> (SER, BER)
+REPLICA = {8: ("0.2408", "0.0488"), 16: ("0.2382", "0.0484"), 32: ("0.2279", "0.0468"),
+           64: ("0.2166", "0.0456"), 128: ("0.1968", "0.0415")}
+
+
+def _half_ulp(s: str) -> float:
+    """Half a unit of the last printed digit of a table entry."""
+    if "." not in s:
+        return 0.5
+    return 0.5 * 10.0 ** (-len(s.split(".")[1]))
+
+
+def _check(rows, table, n_sym, n_bit, mode):
+    by = {(r.detector, r.snr_db): r for r in rows}
+    snrs = sorted({r.snr_db for r in rows})
+    for det, vals in table.items():
+        for snr, (ser_s, ber_s) in zip(snrs, vals):
+            r = by[(det, snr)]
+            for got, want_s, n in ((r.ser, ser_s, n_sym), (r.ber, ber_s, n_bit)):
+                want = float(want_s)
+                if mode == "exact":
+                    assert abs(got - want) <= _half_ulp(want_s) * 1.0001, (det, snr, got, want_s)
+                else:  # binomial 95% CI of the reference value (+ rounding of the table)
+                    ci = 1.96 * math.sqrt(max(want * (1 - want), 1.0 / n) / n) + _half_ulp(want_s)
+                    assert abs(got - want) <= ci, (det, snr, got, want_s, ci)
+
+
+@pytest.fixture(scope="module")
+def harness(built_lib):
+    from paper_2510_01579_b200 import harness
+    return harness
+
+
+@pytest.mark.parametrize("precision", ["fp64_exact", "fp32"])
+@pytest.mark.parametrize("name", sorted(TABLES))
+def test_uplink_curves(name, precision, harness):
+    over, table = TABLES[name]
+    cfg = dataclasses.replace(harness.ExperimentConfig(), mode="uplink_sweep", seed=1,
+                              detectors=tuple(table), **over)
+    rows = harness.run_detection_sweep(cfg, precision=precision)
+    bps = int(round(math.log2(cfg.modulation)))
+    n_sym = cfg.n_trials * cfg.n_t
+    _check(rows, table, n_sym, n_sym * bps, "exact" if precision == "fp64_exact" else "ci")
+
+
+@pytest.mark.parametrize("precision", ["fp64_exact", "fp32"])
+def test_downlink_curves(precision, harness):
+    over, table = DOWNLINK
+    cfg = dataclasses.replace(harness.ExperimentConfig(), seed=1, **over)
+    rows = harness.run_precoding_sweep(cfg, precision=precision)
+    n_sym = cfg.n_trials * cfg.n_r
+    _check(rows, table, n_sym, n_sym * 4, "exact" if precision == "fp64_exact" else "ci")
+
+
+def test_ml_floor_cfg1(harness):
+    cfg = dataclasses.replace(harness.ExperimentConfig(), mode="uplink_sweep", seed=1, n_r=8,
+                              n_t=8, modulation=4, snr_grid_db=SNR, n_trials=896,
+                              detectors=("ml",))
+    rows = harness.run_detection_sweep(cfg)
+    want = {0.0: "0.3982", 5.0: "0.1987", 10.0: "0.0167", 15.0: "0", 20.0: "0", 25.0: "0"}
+    for r in rows:
+        assert abs(r.ser - float(want[r.snr_db])) <= _half_ulp(want[r.snr_db]) * 1.0001, r
+
+
+@pytest.mark.parametrize("precision", ["fp64_exact", "fp32"])
+def test_replica_sweep_cfg5(precision, harness):
+    base = dataclasses.replace(harness.ExperimentConfig(), mode="uplink_sweep", seed=1, n_r=16,
+                               n_t=16, modulation=64, snr_grid_db=(30.0,), n_trials=800,
+                               detectors=("cim",))
+    for na, (ser_s, ber_s) in REPLICA.items():
+        cfg = dataclasses.replace(base, cac=dataclasses.replace(base.cac, n_anneals=na))
+        (r,) = harness.run_detection_sweep(cfg, precision=precision)
+        n_sym = 800 * 16
+        _check([r], {"cim": [(ser_s, ber_s)]}, n_sym, n_sym * 6,
+               "exact" if precision == "fp64_exact" else "ci")
