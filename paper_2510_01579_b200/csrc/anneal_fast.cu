@@ -59,13 +59,13 @@ constexpr int kWarpsPerCta = 4;
 #define IL_NOUTER 0
 #endif
 #ifndef IL_PB2  // packed partial sums for the aux coupling
-#define IL_PB2 0
+#define IL_PB2 1
 #endif
-#ifndef IL_LAZY_FLOOR  // one min per step decides whether the e floor binds
-#define IL_LAZY_FLOOR 0
+#ifndef IL_BOUND_FLOOR  // per-thread lower bound on e replaces per-spin floor checks
+#define IL_BOUND_FLOOR 1
 #endif
-#if IL_LAZY_FLOOR && IL_FUSE1
-#error "IL_LAZY_FLOOR is implemented for the default loop structure only"
+#if IL_BOUND_FLOOR && (IL_FUSE1 || IL_LOOP2)
+#error "IL_BOUND_FLOOR is implemented for the default loop structure only"
 #endif
 
 struct FastScalars {
@@ -130,8 +130,8 @@ __device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
     const float2 t = __fmul2_rn(x, q);
     x = __ffma2_rn(e, C, t);
     const float2 er = __fmul2_rn(e, r);
-#if IL_LAZY_FLOOR
-    // floor applied by the caller only if some e of the step fell below it
+#if IL_BOUND_FLOOR
+    // floor applied by the caller only if some e of the step may fall below it
     e = er;
     (void)e_floor;
 #else
@@ -139,12 +139,6 @@ __device__ __forceinline__ void euler_pair(float2& x, float2& e, const float2 C,
 #endif
 }
 
-__device__ __forceinline__ float min_nan3(float a, float b, float c) {
-    float r;
-    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
-    asm("min.NaN.f32 %0, %0, %1;" : "+f"(r) : "f"(c));
-    return r;
-}
 __device__ __forceinline__ float2 floor2(float2 e, float f) {
     return make_float2(fmaxf(e.x, f), fmaxf(e.y, f));
 }
@@ -245,6 +239,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     }
     float xa = x0s[(g + 8 * hown) * S + 2 * N], ea = e_init, Ca = 0.f, dva = 0.f;
     float dv[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+#if IL_BOUND_FLOOR
+    float e_lb = e_init;  // lower bound of every eA/eB of this thread
+#endif
     __syncwarp();
 
     // ---- stage -Ks*G as f16 B fragments (hi, lo) of m16n8k16 --------------
@@ -435,21 +432,21 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
             }
         }
-#if IL_LAZY_FLOOR
-        // e' = max(e_floor, e q): one NaN-propagating min over the step's new
-        // e values decides whether any floor binds (rare: e starts at 1 and
-        // shrinks only where x^2 > a); the result is identical to clamping
-        // every element, a NaN e takes the clamping path as before
+#if IL_BOUND_FLOOR
+        // e' = max(e_floor, e r).  Every e of this thread stays >= e_lb, a
+        // lower bound advanced per step with the smallest factor any of its
+        // spins can have: r_i = fma(-dt zeta, x2_i, beta) >= fma(-dt zeta, dmax,
+        // beta) since x2_i <= dmax (the sticky max of x^2 already tracked for
+        // divergence) and rounding is monotone.  While e_lb r_lb >= e_floor no
+        // floor can bind and the 2 FMNMX per spin pair are skipped; otherwise
+        // every element is clamped exactly as before (also for NaN).
         {
-            float em = INFINITY;
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int n = 0; n < NT; ++n) {
-                    em = min_nan3(em, eA[h][n].x, eA[h][n].y);
-                    em = min_nan3(em, eB[h][n].x, eB[h][n].y);
-                }
-            if (!(em >= e_floor)) {
+            const float dmax = max_nan3(max_nan(dv[0][0], dv[0][1]), dv[1][0], dv[1][1]);
+            const float r_lb = SAME_QR ? fmaf(s.ndt, dmax, s.alpha) : fmaf(s.ndtz, dmax, s.beta);
+            const float nxt = e_lb * r_lb;
+            if (nxt >= e_floor) {
+                e_lb = nxt;
+            } else {
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -457,6 +454,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                         eA[h][n] = floor2(eA[h][n], e_floor);
                         eB[h][n] = floor2(eB[h][n], e_floor);
                     }
+                e_lb = e_floor;
             }
         }
 #endif
