@@ -10,30 +10,40 @@
 // required for the overlap (pageable memory works but the copies then
 // serialise with the host thread; pageable outputs only delay the tail).
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "il_internal.cuh"
 
 using namespace il;
 
+#ifndef IL_PIPE_CAP_DIV
+#define IL_PIPE_CAP_DIV 16
+#endif
+
 namespace {
 
+// Streams and events of the pipeline, created once per device and reused:
+// creating 4 streams and 2 x n_chunks events per call cost ~0.4 ms.  Calls
+// are serialised by the mutex (the pipeline owns its streams for the call).
 struct Streams {
     cudaStream_t in = nullptr, out = nullptr, comp[2] = {nullptr, nullptr};
     std::vector<cudaEvent_t> ev;
-    ~Streams() {
-        for (cudaEvent_t e : ev) cudaEventDestroy(e);
-        for (cudaStream_t s : {in, out, comp[0], comp[1]})
-            if (s) cudaStreamDestroy(s);
-    }
     int init(int n_events) {
-        for (cudaStream_t* s : {&in, &out, &comp[0], &comp[1]})
-            IL_CHECK_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
-        ev.resize(n_events, nullptr);
-        for (auto& e : ev) IL_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (!in)
+            for (cudaStream_t* s : {&in, &out, &comp[0], &comp[1]})
+                IL_CHECK_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+        while ((int)ev.size() < n_events) {
+            cudaEvent_t e;
+            IL_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            ev.push_back(e);
+        }
         return IL_OK;
     }
 };
+
+std::mutex g_pipe_mu;
+Streams g_pipe[64];  // per device ordinal
 
 void keep_pool_warm() {
     static bool done = false;
@@ -59,13 +69,32 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
     IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && x_idx), "NULL buffer");
     if (P == 0) return IL_OK;
     keep_pool_warm();
-    if (n_chunks <= 0) n_chunks = P >= 32768 ? 12 : (P >= 16384 ? 8 : (P >= 4096 ? 4 : 1));
-    n_chunks = (int)std::min<int64_t>(std::min(n_chunks, 64), P);
-    int64_t chunk = (P + n_chunks - 1) / n_chunks;
-    chunk = (chunk + 7) / 8 * 8;
-    n_chunks = (int)((P + chunk - 1) / chunk);
+    // chunk boundaries: n_chunks > 0 -> equal chunks; otherwise (P >= 4096)
+    // a ramp: a small first chunk (~P/48, its H2D is the exposed latency)
+    // doubling up to P/16, so few chunks carry wave tails
+    std::vector<int64_t> bounds{0};
+    if (n_chunks > 0 || P < 4096) {
+        if (n_chunks <= 0) n_chunks = 1;
+        n_chunks = (int)std::min<int64_t>(std::min(n_chunks, 64), P);
+        int64_t chunk = (P + n_chunks - 1) / n_chunks;
+        chunk = (chunk + 7) / 8 * 8;
+        while (bounds.back() < P) bounds.push_back(std::min(P, bounds.back() + chunk));
+    } else {
+        const int64_t cap = std::max<int64_t>(P / IL_PIPE_CAP_DIV, 8);
+        int64_t c = std::max<int64_t>(P / 48, 256);
+        while (bounds.back() < P) {
+            const int64_t cc = (std::min(c, cap) + 7) / 8 * 8;
+            bounds.push_back(std::min(P, bounds.back() + cc));
+            c *= 2;
+        }
+    }
+    n_chunks = (int)bounds.size() - 1;
 
-    Streams ss;
+    int dev_id = 0;
+    IL_CHECK_CUDA(cudaGetDevice(&dev_id));
+    IL_REQUIRE(dev_id < 64, "device ordinal out of range");
+    std::lock_guard<std::mutex> lock(g_pipe_mu);
+    Streams& ss = g_pipe[dev_id];
     int rc = ss.init(2 * n_chunks + 1);
     if (rc) return rc;
     const size_t hsz = (size_t)n_r * n_t * 2, ysz = (size_t)n_r * 2, xsz = (size_t)n_t * 2;
@@ -97,7 +126,7 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
         cudaStreamWaitEvent(ss.comp[1], ready, 0);
         cudaStreamWaitEvent(ss.out, ready, 0);
         for (int c = 0; c < n_chunks && rc == IL_OK; ++c) {
-            const int64_t o = c * chunk, n = std::min(chunk, P - o);
+            const int64_t o = bounds[c], n = bounds[c + 1] - o;
             cudaMemcpyAsync(dH + o * hsz, H + o * hsz, sizeof(double) * hsz * n,
                             cudaMemcpyHostToDevice, ss.in);
             cudaMemcpyAsync(dy + o * ysz, y + o * ysz, sizeof(double) * ysz * n,
@@ -119,7 +148,7 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
         // into pageable memory blocks the host thread, which must not delay
         // the enqueue of later chunks (the outputs are ~1% of the inputs)
         for (int c = 0; c < n_chunks && rc == IL_OK; ++c) {
-            const int64_t o = c * chunk, n = std::min(chunk, P - o);
+            const int64_t o = bounds[c], n = bounds[c + 1] - o;
             cudaStreamWaitEvent(ss.out, ss.ev[2 * c + 1], 0);
             cudaMemcpyAsync(x_idx + o * xsz, dx + o * xsz, xsz * n, cudaMemcpyDeviceToHost, ss.out);
             if (energy)
