@@ -132,10 +132,19 @@ def residual_energy(H: np.ndarray, y: np.ndarray, x: np.ndarray) -> float:
 # ---------------------------------------------------------------------------
 # linear front-end and Ising reduction
 # ---------------------------------------------------------------------------
-def detect_mmse(inst: MimoInstance) -> DetectionResult:
-    """linear.py:69-75 on the GPU."""
+def _check_uplink(inst: MimoInstance) -> None:
+    """linear.py:50-52, plus SciPy's check_finite of the Cholesky solve: the
+    reference raises ValueError on non-finite H, y or noise variance."""
     if inst.n_r < inst.n_t:
         raise ValueError("uplink detection requires n_r >= n_t")
+    if not (np.all(np.isfinite(inst.H)) and np.all(np.isfinite(inst.y))
+            and np.isfinite(inst.noise_var)):
+        raise ValueError("array must not contain infs or NaNs")
+
+
+def detect_mmse(inst: MimoInstance) -> DetectionResult:
+    """linear.py:69-75 on the GPU."""
+    _check_uplink(inst)
     x_idx, energy, status = batched.mmse_batch(inst.H[None], inst.y[None],
                                                np.array([inst.noise_var]),
                                                _order_code(inst.constellation))
@@ -147,8 +156,7 @@ def detect_mmse(inst: MimoInstance) -> DetectionResult:
 
 def detect_mmse_sic(inst: MimoInstance) -> DetectionResult:
     """linear.py:78-106 (ordered MMSE-SIC) on the GPU."""
-    if inst.n_r < inst.n_t:
-        raise ValueError("uplink detection requires n_r >= n_t")
+    _check_uplink(inst)
     x_idx, energy, status = batched.mmse_sic_batch(inst.H[None], inst.y[None],
                                                    np.array([inst.noise_var]),
                                                    _order_code(inst.constellation))
@@ -156,6 +164,20 @@ def detect_mmse_sic(inst: MimoInstance) -> DetectionResult:
         raise np.linalg.LinAlgError("regularized normal matrix is not positive definite")
     x = from_indices(x_idx[0].cpu().numpy(), inst.constellation)
     return DetectionResult(x_hard=x, energy=float(energy[0]), source="mmse_sic")
+
+
+ML_MAX_BITS = 24  # linear.py:28
+
+
+def detect_ml(inst: MimoInstance) -> DetectionResult:
+    """linear.py:109-144: exhaustive ML on the GPU (ties to the smallest
+    symbol-index vector, user 0 most significant)."""
+    bits = inst.n_t * inst.constellation.bits_per_symbol
+    if bits > ML_MAX_BITS:
+        raise ValueError(f"ML search space of {bits} bits exceeds the {ML_MAX_BITS}-bit guard")
+    x_idx, energy = batched.ml_batch(inst.H[None], inst.y[None], _order_code(inst.constellation))
+    x = from_indices(x_idx[0].cpu().numpy(), inst.constellation)
+    return DetectionResult(x_hard=x, energy=float(energy[0]), source="ml")
 
 
 def build_ising(inst: MimoInstance, x_guess: np.ndarray) -> StructuredIsing:
@@ -287,8 +309,7 @@ def detect_cim(inst: MimoInstance, params=None, seed: int = 0, counters=None) ->
                                    diverged_count=diverged)
         return DetectionResult(x_hard=x, energy=energy, source="anneal", anneal_index=widx,
                                diverged_count=diverged)
-    if inst.n_r < inst.n_t:
-        raise ValueError("uplink detection requires n_r >= n_t")
+    _check_uplink(inst)
     r = batched.detect_cim_batch(inst.H[None], inst.y[None], np.array([inst.noise_var]),
                                  _order_code(inst.constellation), np.array([seed], np.uint64),
                                  params)
@@ -337,8 +358,7 @@ def detect_cim_multi(inst: MimoInstance, params=None, n_stages: int = 1, seed: i
                                        anneal_index=widx)
         return DetectionResult(x_hard=best.x_hard, energy=best.energy, source=best.source,
                                anneal_index=best.anneal_index, diverged_count=total)
-    if inst.n_r < inst.n_t:
-        raise ValueError("uplink detection requires n_r >= n_t")
+    _check_uplink(inst)
     r = batched.detect_cim_multi_batch(inst.H[None], inst.y[None], np.array([inst.noise_var]),
                                        _order_code(inst.constellation),
                                        np.array([seed], np.uint64), params, n_stages, chains)

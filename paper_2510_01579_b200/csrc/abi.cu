@@ -256,7 +256,7 @@ int il_detect_cim_batch(const double* H, const double* y, const double* noise_va
     if (rc) return rc;
     IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
                "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
-    IL_REQUIRE(x_idx != nullptr, "x_idx must not be NULL");
+    IL_REQUIRE(P == 0 || x_idx != nullptr, "x_idx must not be NULL");
     Alphabet al;
     rc = make_qam_alphabet(qam_order, &al);
     if (rc) return rc;

@@ -32,6 +32,9 @@ constexpr int kRowsThreads = 128;
 #define IL_GRAM_UNROLL 1
 #endif
 constexpr int kGramUnroll = IL_GRAM_UNROLL;
+#ifndef IL_PROBE_NO_LAMBDA
+#define IL_PROBE_NO_LAMBDA 0
+#endif
 
 // Per-group shared-memory slice (cplx units).
 IL_HD size_t rows_group_cplx(int n_r, int n, int GS) {
@@ -291,7 +294,11 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
                 tr = 2.0 * gi;
             }
             tr = g.sum(tr);
+#if IL_PROBE_NO_LAMBDA  // timing probe only: skips lambda_max (wrong eps)
+            const double lam_a = 1.0;
+#else
             const double lam_a = lambda_max_rows<GS>(g, A, n, vb, wb, dsm, esm);
+#endif
             if (r == 0) {
                 const double lam = c2 * lam_a;
                 const double S = (double)(2 * N + 1);
