@@ -61,6 +61,9 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_PB2  // packed partial sums for the aux coupling
 #define IL_PB2 1
 #endif
+#ifndef IL_FHFMA_SPLIT  // f16 hi/lo split residual via mixed-precision FMA
+#define IL_FHFMA_SPLIT 1
+#endif
 #ifndef IL_BOUND_FLOOR  // per-thread lower bound on e replaces per-spin floor checks
 #define IL_BOUND_FLOOR 1
 #endif
@@ -86,10 +89,22 @@ __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cas
 // hi + lo split of a float pair into two packed f16x2 words (x in the low half)
 __device__ __forceinline__ void split_h2(float2 v, uint32_t& hi, uint32_t& lo) {
     const __half2 h = __float22half2_rn(v);
+    hi = h2_bits(h);
+#if IL_FHFMA_SPLIT
+    // residual v - f32(hi) by a mixed-precision FMA straight from the f16
+    // halves (hi * -1 + v, exact): 2 FHFMA instead of 2 HADD2.F32 + 1 FADD2
+    float r0, r1;
+    asm("{\n .reg .b16 a, b;\n mov.b32 {a, b}, %2;\n"
+        " fma.rn.f32.f16 %0, a, %4, %3;\n"
+        " fma.rn.f32.f16 %1, b, %4, %5;\n}"
+        : "=f"(r0), "=f"(r1)
+        : "r"(hi), "f"(v.x), "h"((unsigned short)0xBC00), "f"(v.y));
+    lo = h2_bits(__float22half2_rn(make_float2(r0, r1)));
+#else
     const float2 hf = __half22float2(h);
     const float2 r = __fadd2_rn(v, make_float2(-hf.x, -hf.y));
-    hi = h2_bits(h);
     lo = h2_bits(__float22half2_rn(r));
+#endif
 }
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0,
