@@ -211,6 +211,14 @@ int il_detect_cim_host(const double* H, const double* y, const double* noise_var
                        double* energy, int8_t* source, int32_t* anneal_index,
                        int32_t* diverged_count, int32_t n_chunks);
 
+/* Host-buffer form of il_precode_vpp_batch (every pointer HOST memory),
+ * streamed through the device in n_chunks pieces (<= 0: auto) like
+ * il_detect_cim_host. */
+int il_precode_vpp_host(const double* H, const double* u, int64_t P, int32_t n_u,
+                        int32_t n_ant, double power, double tau, int32_t n_stages,
+                        const uint64_t* seed, const il_cac_params* prm, double* x, double* v,
+                        double* unnorm_power, int32_t* diverged_count, int32_t n_chunks);
+
 /* ---------------------------------------------------------------------------
  * Batched downlink vector-perturbation precoding: P x precode_vpp
  * (precoder.py:93-146).  H [P, n_u, n_ant] complex128 (n_u <= n_ant),

@@ -61,6 +61,9 @@ _SIGS = {
     "il_detect_cim_host": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
                             ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _c_i32],
                            ctypes.c_int),
+    "il_precode_vpp_host": ([_vp, _vp, _c_i64, _c_i32, _c_i32, _c_d, _c_d, _c_i32, _vp,
+                             ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _c_i32],
+                            ctypes.c_int),
     "il_precode_vpp_batch": ([_vp, _vp, _c_i64, _c_i32, _c_i32, _c_d, _c_d, _c_i32, _vp,
                               ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp],
                              ctypes.c_int),

@@ -171,6 +171,32 @@ def precode_vpp_batch(H, u, power: float, tau: float, seeds, params=None, n_stag
     return out
 
 
+def precode_vpp_host(H, u, power: float, tau: float, seeds, params=None, n_stages: int = 1,
+                     precision: str | None = None, n_chunks: int = 0) -> PrecodeBatch:
+    """P x ``precode_vpp`` from HOST buffers to HOST buffers, streamed through
+    the GPU in chunks with copies overlapped (il_precode_vpp_host)."""
+    params = params or CacParams()
+    prm = to_c(params, precision)
+    Ht = H if isinstance(H, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(H))
+    if Ht.dim() != 3:
+        raise ValueError("H must be [P, n_u, n_ant]")
+    P, n_u, n_ant = Ht.shape
+    Hh = _host(Ht, torch.complex128, (P, n_u, n_ant))
+    uh = _host(u, torch.complex128, (P, n_u))
+    st = seeds if isinstance(seeds, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1)))
+    st = _host(st, st.dtype, (P,))
+    pin = torch.cuda.is_available()
+    out = PrecodeBatch(x=torch.empty((P, n_ant), dtype=torch.complex128, pin_memory=pin),
+                       v=torch.empty((P, n_u), dtype=torch.complex128, pin_memory=pin),
+                       unnormalized_power=torch.empty(P, dtype=torch.float64, pin_memory=pin),
+                       diverged=torch.empty(P, dtype=torch.int32, pin_memory=pin))
+    _lib.call("il_precode_vpp_host", Hh.data_ptr(), uh.data_ptr(), P, n_u, n_ant, float(power),
+              float(tau), int(n_stages), st.data_ptr(), prm, out.x.data_ptr(), out.v.data_ptr(),
+              out.unnormalized_power.data_ptr(), out.diverged.data_ptr(), int(n_chunks))
+    return out
+
+
 def mmse_batch(H, y, noise_var, order: int):
     """P x ``detect_mmse`` (linear.py:55-75) -> (x_idx, energy, status)."""
     Hd = _dev(H, torch.complex128)

@@ -57,21 +57,18 @@ void keep_pool_warm() {
     done = true;
 }
 
-}  // namespace
+// One per-item array moved between host and device: `bytes` per problem.
+struct PipeBuf {
+    const void* host_in;   // input (H2D) or nullptr
+    void* host_out;        // output (D2H) or nullptr
+    size_t bytes;
+    char* dev = nullptr;
+};
 
-extern "C" int il_detect_cim_host(const double* H, const double* y, const double* noise_var,
-                                  int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
-                                  const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
-                                  double* energy, int8_t* source, int32_t* anneal_index,
-                                  int32_t* diverged_count, int32_t n_chunks) {
-    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
-               "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
-    IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && x_idx), "NULL buffer");
-    if (P == 0) return IL_OK;
-    keep_pool_warm();
-    // chunk boundaries: n_chunks > 0 -> equal chunks; otherwise (P >= 4096)
-    // a ramp: a small first chunk (~P/48, its H2D is the exposed latency)
-    // doubling up to P/16, so few chunks carry wave tails
+// Chunk boundaries: n_chunks > 0 -> equal chunks; otherwise (P >= 4096) a
+// ramp: a small first chunk (~P/48, its H2D is the exposed latency) doubling
+// up to P/16, so few chunks carry wave tails.
+std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
     std::vector<int64_t> bounds{0};
     if (n_chunks > 0 || P < 4096) {
         if (n_chunks <= 0) n_chunks = 1;
@@ -88,91 +85,114 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
             c *= 2;
         }
     }
-    n_chunks = (int)bounds.size() - 1;
+    return bounds;
+}
 
+// The chunked pipeline: H2D of every input chunk on `in`, compute(o, n, s)
+// on alternating compute streams once its inputs landed, D2H of the outputs
+// on `out` (enqueued last: a copy into pageable memory blocks the host
+// thread and must not delay the enqueue of later chunks).
+template <class F>
+int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& compute) {
+    keep_pool_warm();
+    const std::vector<int64_t> bounds = chunk_bounds(P, n_chunks);
+    const int K = (int)bounds.size() - 1;
     int dev_id = 0;
     IL_CHECK_CUDA(cudaGetDevice(&dev_id));
     IL_REQUIRE(dev_id < 64, "device ordinal out of range");
     std::lock_guard<std::mutex> lock(g_pipe_mu);
     Streams& ss = g_pipe[dev_id];
-    int rc = ss.init(2 * n_chunks + 1);
+    int rc = ss.init(2 * K + 1);
     if (rc) return rc;
-    const size_t hsz = (size_t)n_r * n_t * 2, ysz = (size_t)n_r * 2, xsz = (size_t)n_t * 2;
-    // device buffers for the whole slot (stream-ordered on `in`; the other
-    // streams are ordered after the allocation through the first event)
-    double *dH = nullptr, *dy = nullptr, *ds2 = nullptr, *den = nullptr;
-    uint64_t* dseed = nullptr;
-    uint8_t* dx = nullptr;
-    int8_t* dsrc = nullptr;
-    int32_t *dai = nullptr, *ddc = nullptr;
-    auto alloc = [&](void** p, size_t bytes) {
-        if (rc) return;
-        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 1, ss.in);
-        if (e != cudaSuccess) rc = fail_cuda(e, "cudaMallocAsync(il_detect_cim_host)");
-    };
-    alloc((void**)&dH, sizeof(double) * hsz * P);
-    alloc((void**)&dy, sizeof(double) * ysz * P);
-    alloc((void**)&ds2, sizeof(double) * P);
-    alloc((void**)&dseed, sizeof(uint64_t) * P);
-    alloc((void**)&dx, xsz * P);
-    alloc((void**)&den, sizeof(double) * P);
-    alloc((void**)&dsrc, P);
-    alloc((void**)&dai, sizeof(int32_t) * P);
-    alloc((void**)&ddc, sizeof(int32_t) * P);
+    for (PipeBuf& b : bufs) {  // stream-ordered on `in`, published by the first event
+        if (rc) break;
+        cudaError_t e = cudaMallocAsync((void**)&b.dev, b.bytes * P, ss.in);
+        if (e != cudaSuccess) rc = fail_cuda(e, "cudaMallocAsync(pipeline)");
+    }
     if (rc == IL_OK) {
-        cudaEvent_t ready = ss.ev[2 * n_chunks];
+        cudaEvent_t ready = ss.ev[2 * K];
         cudaEventRecord(ready, ss.in);
         cudaStreamWaitEvent(ss.comp[0], ready, 0);
         cudaStreamWaitEvent(ss.comp[1], ready, 0);
         cudaStreamWaitEvent(ss.out, ready, 0);
-        for (int c = 0; c < n_chunks && rc == IL_OK; ++c) {
+        for (int c = 0; c < K && rc == IL_OK; ++c) {
             const int64_t o = bounds[c], n = bounds[c + 1] - o;
-            cudaMemcpyAsync(dH + o * hsz, H + o * hsz, sizeof(double) * hsz * n,
-                            cudaMemcpyHostToDevice, ss.in);
-            cudaMemcpyAsync(dy + o * ysz, y + o * ysz, sizeof(double) * ysz * n,
-                            cudaMemcpyHostToDevice, ss.in);
-            cudaMemcpyAsync(ds2 + o, noise_var + o, sizeof(double) * n, cudaMemcpyHostToDevice,
-                            ss.in);
-            cudaMemcpyAsync(dseed + o, seed + o, sizeof(uint64_t) * n, cudaMemcpyHostToDevice,
-                            ss.in);
+            for (PipeBuf& b : bufs)
+                if (b.host_in)
+                    cudaMemcpyAsync(b.dev + o * b.bytes, (const char*)b.host_in + o * b.bytes,
+                                    n * b.bytes, cudaMemcpyHostToDevice, ss.in);
             cudaEventRecord(ss.ev[2 * c], ss.in);
             cudaStream_t cs = ss.comp[c & 1];
             cudaStreamWaitEvent(cs, ss.ev[2 * c], 0);
-            rc = il_detect_cim_batch(dH + o * hsz, dy + o * ysz, ds2 + o, n, n_r, n_t, qam_order,
-                                     dseed + o, prm, dx + o * xsz, den + o, dsrc + o, dai + o,
-                                     ddc + o, cs);
+            rc = compute(o, n, cs);
             if (rc) break;
             cudaEventRecord(ss.ev[2 * c + 1], cs);
         }
-        // D2H copies are enqueued after every chunk's H2D and compute: a copy
-        // into pageable memory blocks the host thread, which must not delay
-        // the enqueue of later chunks (the outputs are ~1% of the inputs)
-        for (int c = 0; c < n_chunks && rc == IL_OK; ++c) {
+        for (int c = 0; c < K && rc == IL_OK; ++c) {
             const int64_t o = bounds[c], n = bounds[c + 1] - o;
             cudaStreamWaitEvent(ss.out, ss.ev[2 * c + 1], 0);
-            cudaMemcpyAsync(x_idx + o * xsz, dx + o * xsz, xsz * n, cudaMemcpyDeviceToHost, ss.out);
-            if (energy)
-                cudaMemcpyAsync(energy + o, den + o, sizeof(double) * n, cudaMemcpyDeviceToHost,
-                                ss.out);
-            if (source) cudaMemcpyAsync(source + o, dsrc + o, n, cudaMemcpyDeviceToHost, ss.out);
-            if (anneal_index)
-                cudaMemcpyAsync(anneal_index + o, dai + o, sizeof(int32_t) * n,
-                                cudaMemcpyDeviceToHost, ss.out);
-            if (diverged_count)
-                cudaMemcpyAsync(diverged_count + o, ddc + o, sizeof(int32_t) * n,
-                                cudaMemcpyDeviceToHost, ss.out);
+            for (PipeBuf& b : bufs)
+                if (b.host_out)
+                    cudaMemcpyAsync((char*)b.host_out + o * b.bytes, b.dev + o * b.bytes,
+                                    n * b.bytes, cudaMemcpyDeviceToHost, ss.out);
         }
     }
     // frees are ordered after every use: join the compute streams into `out`
-    cudaEvent_t done0 = ss.ev[0], done1 = ss.ev[1];
-    cudaEventRecord(done0, ss.comp[0]);
-    cudaEventRecord(done1, ss.comp[1]);
-    cudaStreamWaitEvent(ss.out, done0, 0);
-    cudaStreamWaitEvent(ss.out, done1, 0);
-    for (void* p : {(void*)dH, (void*)dy, (void*)ds2, (void*)dseed, (void*)dx, (void*)den,
-                    (void*)dsrc, (void*)dai, (void*)ddc})
-        if (p) cudaFreeAsync(p, ss.out);
+    cudaEventRecord(ss.ev[0], ss.comp[0]);
+    cudaEventRecord(ss.ev[1], ss.comp[1]);
+    cudaStreamWaitEvent(ss.out, ss.ev[0], 0);
+    cudaStreamWaitEvent(ss.out, ss.ev[1], 0);
+    for (PipeBuf& b : bufs)
+        if (b.dev) cudaFreeAsync(b.dev, ss.out);
     cudaError_t e = cudaStreamSynchronize(ss.out);
-    if (rc == IL_OK && e != cudaSuccess) rc = fail_cuda(e, "il_detect_cim_host");
+    if (rc == IL_OK && e != cudaSuccess) rc = fail_cuda(e, "host pipeline");
     return rc;
+}
+
+}  // namespace
+
+extern "C" int il_detect_cim_host(const double* H, const double* y, const double* noise_var,
+                                  int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                                  const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
+                                  double* energy, int8_t* source, int32_t* anneal_index,
+                                  int32_t* diverged_count, int32_t n_chunks) {
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
+               "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
+    IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && x_idx), "NULL buffer");
+    if (P == 0) return IL_OK;
+    std::vector<PipeBuf> b = {
+        {H, nullptr, sizeof(double) * 2 * n_r * n_t}, {y, nullptr, sizeof(double) * 2 * n_r},
+        {noise_var, nullptr, sizeof(double)},         {seed, nullptr, sizeof(uint64_t)},
+        {nullptr, x_idx, (size_t)2 * n_t},            {nullptr, energy, sizeof(double)},
+        {nullptr, source, 1},                         {nullptr, anneal_index, sizeof(int32_t)},
+        {nullptr, diverged_count, sizeof(int32_t)}};
+    return run_pipeline(P, n_chunks, b, [&](int64_t o, int64_t n, cudaStream_t cs) {
+        auto at = [&](int k) { return b[k].dev + o * b[k].bytes; };
+        return il_detect_cim_batch((const double*)at(0), (const double*)at(1),
+                                   (const double*)at(2), n, n_r, n_t, qam_order,
+                                   (const uint64_t*)at(3), prm, (uint8_t*)at(4), (double*)at(5),
+                                   (int8_t*)at(6), (int32_t*)at(7), (int32_t*)at(8), cs);
+    });
+}
+
+extern "C" int il_precode_vpp_host(const double* H, const double* u, int64_t P, int32_t n_u,
+                                   int32_t n_ant, double power, double tau, int32_t n_stages,
+                                   const uint64_t* seed, const il_cac_params* prm, double* x,
+                                   double* v, double* unnorm_power, int32_t* diverged_count,
+                                   int32_t n_chunks) {
+    IL_REQUIRE(P >= 0 && n_u >= 1 && n_u <= n_ant, "downlink precoding requires 1 <= n_u <= n_ant");
+    IL_REQUIRE(P == 0 || (H && u && seed && prm && x && v), "NULL buffer");
+    if (P == 0) return IL_OK;
+    std::vector<PipeBuf> b = {
+        {H, nullptr, sizeof(double) * 2 * n_u * n_ant}, {u, nullptr, sizeof(double) * 2 * n_u},
+        {seed, nullptr, sizeof(uint64_t)},              {nullptr, x, sizeof(double) * 2 * n_ant},
+        {nullptr, v, sizeof(double) * 2 * n_u},         {nullptr, unnorm_power, sizeof(double)},
+        {nullptr, diverged_count, sizeof(int32_t)}};
+    return run_pipeline(P, n_chunks, b, [&](int64_t o, int64_t n, cudaStream_t cs) {
+        auto at = [&](int k) { return b[k].dev + o * b[k].bytes; };
+        return il_precode_vpp_batch((const double*)at(0), (const double*)at(1), n, n_u, n_ant,
+                                    power, tau, n_stages, (const uint64_t*)at(2), prm,
+                                    (double*)at(3), (double*)at(4), (double*)at(5),
+                                    (int32_t*)at(6), cs);
+    });
 }

@@ -250,3 +250,21 @@ def test_fast_kernel_any_replica_count(n_anneals):
                            seed=int(d["seed"][i]))
         want = np.stack([orc.level_index(r["x"].real, levels), orc.level_index(r["x"].imag, levels)], -1)
         assert np.array_equal(ex.x_idx[i].cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("n_chunks", [0, 1, 4])
+def test_precode_vpp_host_pipeline_matches_device_batch(n_chunks):
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    d = load_golden("vpp8x8_16qam.npz")
+    H = np.concatenate([d["H"]] * 3)[:-5]
+    u = np.concatenate([d["u"]] * 3)[:-5]
+    seed = np.concatenate([d["seed"]] * 3)[:-5]
+    prm = CacParams(precision="fp64_exact")
+    dev = batched.precode_vpp_batch(H, u, float(d["P"]), float(d["tau"]), seed, prm)
+    host = batched.precode_vpp_host(H, u, float(d["P"]), float(d["tau"]), seed, prm,
+                                    n_chunks=n_chunks)
+    for f in ("x", "v", "unnormalized_power", "diverged"):
+        assert torch.equal(getattr(dev, f).cpu(), getattr(host, f)), f
+    n = len(d["v"])
+    assert np.array_equal(host.v.numpy()[:n], d["v"])
