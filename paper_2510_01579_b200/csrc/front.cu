@@ -361,6 +361,12 @@ int front_blocks(int64_t P, size_t per_warp, int* wpb, size_t* smem) {
 // ---------------------------------------------------------------------------
 // selection / decode epilogue
 // ---------------------------------------------------------------------------
+IL_HD size_t sel_warp_bytes(int n_r, int n_t, bool with_g) {
+    const size_t N = 2 * (size_t)n_t;
+    const size_t bytes = sizeof(cplx) * ((size_t)n_r * n_t + n_r) + (with_g ? 8 * (N * N + N) : 0);
+    return (bytes + 15) / 16 * 16;
+}
+
 __global__ void k_select_decode(const double* __restrict__ Hg, const double* __restrict__ yg,
                                 const double* __restrict__ Gg, const double* __restrict__ bg,
                                 const double* __restrict__ offset, const int8_t* __restrict__ spins,
@@ -375,26 +381,34 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
     const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (prob >= P) return;
     const int N = 2 * n_t, S = 2 * N + 1;
-    const size_t per_warp = sizeof(double) * ((size_t)N * N + N) + sizeof(cplx) * ((size_t)n_r * n_t + n_r);
-    char* base = smem_raw + warp * ((per_warp + 15) / 16 * 16);
-    double* G = reinterpret_cast<double*>(base);
-    double* b = G + N * N;
-    cplx* H = reinterpret_cast<cplx*>(b + N);
+    // per-warp slice: H, y, then (only without precomputed energies) G, b
+    const size_t per_warp = sel_warp_bytes(n_r, n_t, energies == nullptr);
+    char* base = smem_raw + warp * per_warp;
+    cplx* H = reinterpret_cast<cplx*>(base);
     cplx* y = H + n_r * n_t;
-    const double* Gp = Gg + prob * (int64_t)N * N;
-    // G and b are only needed when the anneal kernel did not supply energies
-    if (!energies) {
-        for (int i = lane; i < N * N; i += 32) G[i] = Gp[i];
-        for (int i = lane; i < N; i += 32) b[i] = bg[prob * N + i];
+    double* G = reinterpret_cast<double*>(y + n_r);
+    double* b = G + N * N;
+    // H, y (and G, b when the anneal kernel did not supply energies) arrive by
+    // 1-D TMA bulk copies issued by one lane: the warp's loads are in flight
+    // while it reads the energies and flags (every size is a multiple of 16 B)
+    __shared__ __align__(8) uint64_t bars[8];
+    uint64_t* bar = &bars[warp];
+    if (lane == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        const uint32_t hb = (uint32_t)(n_r * n_t * 16), yb = (uint32_t)(n_r * 16);
+        const uint32_t gb = energies ? 0u : (uint32_t)(N * N * 8), bb = energies ? 0u : (uint32_t)(N * 8);
+        mbar_expect_tx(bar, hb + yb + gb + bb);
+        tma_bulk_g2s(H, Hg + prob * (int64_t)n_r * n_t * 2, hb, bar);
+        tma_bulk_g2s(y, yg + prob * (int64_t)n_r * 2, yb, bar);
+        if (!energies) {
+            tma_bulk_g2s(G, Gg + prob * (int64_t)N * N, gb, bar);
+            tma_bulk_g2s(b, bg + prob * (int64_t)N, bb, bar);
+        }
     }
-    {
-        const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n_t;
-        for (int i = lane; i < n_r * n_t; i += 32) H[i] = Hp[i];
-        const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
-        for (int i = lane; i < n_r; i += 32) y[i] = yp[i];
-    }
-    double gsum = 0.0;
     __syncwarp();
+    mbar_wait(bar, 0);
+    double gsum = 0.0;
     if (!energies)
         for (int i = 0; i < N; ++i) gsum += G[i * N + i];
 
@@ -737,8 +751,7 @@ int launch_select_decode(const double* H, const double* y, const double* G, cons
     if (P == 0) return IL_OK;
     const int N = 2 * n_t;
     IL_REQUIRE(2 * n_t <= 128, "n_t too large");
-    const size_t per_warp =
-        ((sizeof(double) * ((size_t)N * N + N) + sizeof(cplx) * ((size_t)n_r * n_t + n_r)) + 15) / 16 * 16;
+    const size_t per_warp = sel_warp_bytes(n_r, n_t, energies == nullptr);
     int wpb = (int)((200 * 1024) / per_warp);
     wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);
     const size_t smem = per_warp * wpb;

@@ -103,6 +103,38 @@ int launch_gray_demap(const uint8_t* x_idx, int64_t n_sym, int bits_per_dim, uin
 int launch_base_seeds(const uint64_t* seed, int64_t P, uint64_t k1, uint64_t k2,
                       uint64_t* base_out, cudaStream_t st);
 
+// ---- TMA bulk copy + mbarrier (sm_90+ PTX, used here on sm_100a) -----------
+IL_D uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+IL_D void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+IL_D void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+IL_D void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+IL_D void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+
 // ---- measurement hooks (prof.cu) -------------------------------------------
 enum ProfKind { kProfFront = 0, kProfAnneal = 1, kProfSelect = 2, kProfOther = 3 };
 int prof_start(int kind, cudaStream_t st);  // counts the launch; events only when profiling
