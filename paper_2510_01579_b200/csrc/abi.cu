@@ -186,37 +186,54 @@ int il_run_anneals_host(const double* G, const double* g_diag, const double* b, 
                         int64_t* steps, int64_t* mvms) {
     IL_REQUIRE(n_dim >= 0 && n_batch >= 0, "negative shape");
     const size_t N = (size_t)n_dim, S = 2 * N + 1, B = (size_t)n_batch;
-    cudaStream_t st;
-    IL_CHECK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-    int rc = IL_OK;
-    {
-        Workspace ws(st);
-        double* dG = ws.get<double>(N * N, &rc);
-        double* dg = ws.get<double>(N, &rc);
-        double* db = ws.get<double>(N, &rc);
-        double* dx = ws.get<double>(B * S, &rc);
-        int8_t* ds = ws.get<int8_t>(B * S, &rc);
-        uint8_t* dd = ws.get<uint8_t>(B, &rc);
-        int64_t* dst = ws.get<int64_t>(B, &rc);
-        int64_t* dm = ws.get<int64_t>(B, &rc);
-        if (rc == IL_OK) {
-            cudaMemcpyAsync(dG, G, N * N * 8, cudaMemcpyHostToDevice, st);
-            cudaMemcpyAsync(dg, g_diag, N * 8, cudaMemcpyHostToDevice, st);
-            cudaMemcpyAsync(db, b, N * 8, cudaMemcpyHostToDevice, st);
-            cudaMemcpyAsync(dx, x0, B * S * 8, cudaMemcpyHostToDevice, st);
-            rc = il_run_anneals(dG, dg, db, dx, n_dim, n_batch, dt, p, a, zeta, eps, e_floor, f_mvm,
-                                n_steps, diverge_threshold, ds, dd, dst, dm, st);
-            if (rc == IL_OK) {
-                cudaMemcpyAsync(spins, ds, B * S, cudaMemcpyDeviceToHost, st);
-                cudaMemcpyAsync(diverged, dd, B, cudaMemcpyDeviceToHost, st);
-                cudaMemcpyAsync(steps, dst, B * 8, cudaMemcpyDeviceToHost, st);
-                cudaMemcpyAsync(mvms, dm, B * 8, cudaMemcpyDeviceToHost, st);
-            }
-        }
+    // one call = one problem (the reference's per-RE granularity): a cached
+    // stream and one pinned staging buffer per thread, so the call is one
+    // H2D copy, the kernel and one D2H copy
+    struct Stage {
+        cudaStream_t st = nullptr;
+        char* host = nullptr;
+        char* dev = nullptr;
+        size_t cap = 0;
+    };
+    static thread_local Stage sg;
+    const size_t in_bytes = 8 * (N * N + 2 * N + B * S);
+    const size_t out_bytes = B * S + B + 16 * B;
+    const size_t need = (in_bytes + out_bytes + 256);
+    if (!sg.st) IL_CHECK_CUDA(cudaStreamCreateWithFlags(&sg.st, cudaStreamNonBlocking));
+    if (need > sg.cap) {
+        if (sg.host) cudaFreeHost(sg.host);
+        if (sg.dev) cudaFree(sg.dev);
+        sg.host = nullptr;
+        sg.dev = nullptr;
+        sg.cap = 0;
+        IL_CHECK_CUDA(cudaMallocHost((void**)&sg.host, need));
+        IL_CHECK_CUDA(cudaMalloc((void**)&sg.dev, need));
+        sg.cap = need;
     }
-    cudaError_t e = cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
-    if (rc == IL_OK && e != cudaSuccess) rc = fail_cuda(e, "il_run_anneals_host");
+    double* h = reinterpret_cast<double*>(sg.host);
+    memcpy(h, G, 8 * N * N);
+    memcpy(h + N * N, g_diag, 8 * N);
+    memcpy(h + N * N + N, b, 8 * N);
+    memcpy(h + N * N + 2 * N, x0, 8 * B * S);
+    const double* d = reinterpret_cast<const double*>(sg.dev);
+    char* dout = sg.dev + (in_bytes + 127) / 128 * 128;
+    char* hout = sg.host + (in_bytes + 127) / 128 * 128;
+    int64_t* dsteps = reinterpret_cast<int64_t*>(dout);
+    int64_t* dmvms = dsteps + B;
+    int8_t* dspins = reinterpret_cast<int8_t*>(dmvms + B);
+    uint8_t* ddiv = reinterpret_cast<uint8_t*>(dspins + B * S);
+    IL_CHECK_CUDA(cudaMemcpyAsync(sg.dev, sg.host, in_bytes, cudaMemcpyHostToDevice, sg.st));
+    int rc = il_run_anneals(d, d + N * N, d + N * N + N, d + N * N + 2 * N, n_dim, n_batch, dt, p,
+                            a, zeta, eps, e_floor, f_mvm, n_steps, diverge_threshold, dspins, ddiv,
+                            dsteps, dmvms, sg.st);
+    if (rc == IL_OK) {
+        IL_CHECK_CUDA(cudaMemcpyAsync(hout, dout, out_bytes, cudaMemcpyDeviceToHost, sg.st));
+        IL_CHECK_CUDA(cudaStreamSynchronize(sg.st));
+        memcpy(steps, hout, 8 * B);
+        memcpy(mvms, hout + 8 * B, 8 * B);
+        memcpy(spins, hout + 16 * B, B * S);
+        memcpy(diverged, hout + 16 * B + B * S, B);
+    }
     return rc;
 }
 
