@@ -120,7 +120,8 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
                              const double* offset, const double* eps, const uint64_t* base,
                              const il_cac_params* prm, uint8_t* x_idx, double* energy,
                              int8_t* source, int32_t* anneal_index, int32_t* diverged_count,
-                             Workspace& ws, cudaStream_t st) {
+                             cudaStream_t st) {
+    Workspace ws(st);  // per stage: released (stream-ordered) when the stage is enqueued
     const int N = 2 * n_t, S = 2 * N + 1, B = prm->n_anneals;
     const AnnealScalars s = scalars_of(prm);
     // the fast kernel runs anneals in tiles of 16: B is padded (anneal r of a
@@ -135,10 +136,12 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
     if (rc) return rc;
     double* energies = nullptr;
     if (fast) {
+        // only the argmin matters here: the kernel screens its anneals in FP32
+        // and evaluates the near-minimal ones in FP64
         energies = ws.get<double>((size_t)P * Bs, &rc);
         if (rc) return rc;
         rc = launch_anneal_fast(G, g, b, base, eps, P, N, Bs, s, prm->precision, spins, div,
-                                energies, st);
+                                energies, st, /*screen_rows=*/B);
     } else {
         rc = launch_anneal_exact(G, g, b, nullptr, base, eps, P, N, B, s, spins, div, nullptr,
                                  nullptr, st);
@@ -297,7 +300,7 @@ int il_detect_cim_batch(const double* H, const double* y, const double* noise_va
     rc = launch_base_seeds(seed, P, 0, 0, base, st);  // detector.py:67 derive_seed(seed, 0, 0)
     if (rc) return rc;
     return anneal_and_select(H, y, P, n_r, n_t, al, G, g, b, off, eps, base, prm, x_idx, en, src,
-                             anneal_index, diverged_count, ws, st);
+                             anneal_index, diverged_count, st);
 }
 
 int il_residual_batch(const double* H, const double* y, const double* x, int64_t P, int32_t n_r,
@@ -400,7 +403,7 @@ int il_detect_cim_multi_batch(const double* H, const double* y, const double* no
             if (rc) return rc;
             IL_CHECK_CUDA(cudaMemsetAsync(ssrc, 0, (size_t)P, st));
             rc = anneal_and_select(H, y, P, n_r, n_t, al, G, g, b, off, eps, base, prm, gx, ge,
-                                   ssrc, sai, sdc, ws, st);
+                                   ssrc, sai, sdc, st);
             if (rc) return rc;
             rc = launch_multi_stage(sai, P, widx, st);
             if (rc) return rc;
@@ -460,7 +463,7 @@ int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_
         rc = launch_base_seeds(seed, P, 0, (uint64_t)stage, base, st);
         if (rc) return rc;
         rc = anneal_and_select(Hp, yt, P, n_ant, n_u, al, G, g, b, off, eps, base, prm, vidx, en,
-                               nullptr, nullptr, stage_div, ws, st);
+                               nullptr, nullptr, stage_div, st);
         if (rc) return rc;
         if (diverged_count) {
             rc = launch_add_i32(stage_div, P, diverged_count, st);

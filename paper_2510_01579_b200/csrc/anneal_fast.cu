@@ -35,6 +35,8 @@
 // yields the -dt*eps*c term of the update.
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
 
@@ -67,6 +69,24 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_BOUND_FLOOR  // per-thread lower bound on e replaces per-spin floor checks
 #define IL_BOUND_FLOOR 1
 #endif
+#ifndef IL_TMA_G  // G, g, b of the CTA's problems staged in shared memory by TMA bulk copies
+#define IL_TMA_G 0  // measured 1% slower: the latency it hides was already covered
+#endif
+#ifndef IL_RNG2  // two interleaved PCG64 chains per lane for the initial states
+#define IL_RNG2 0  // measured 1% slower: the RNG is issue-bound, not latency-bound
+#endif
+#ifndef IL_FUSE_Q  // C-independent half of the first Euler step inside the refresh block
+#define IL_FUSE_Q 0  // measured 1.4% slower (register pressure; bit-identical)
+#endif
+#ifndef IL_PROBE_NO_ENERGY  // timing probe only: skips the FP64 energies (wrong output)
+#define IL_PROBE_NO_ENERGY 0
+#endif
+#ifndef IL_PROBE_NO_RNG  // timing probe only: constant initial states (wrong output)
+#define IL_PROBE_NO_RNG 0
+#endif
+#if IL_FUSE_Q && (IL_FUSE1 || IL_LOOP2)
+#error "IL_FUSE_Q is implemented for the default loop structure only"
+#endif
 #if IL_BOUND_FLOOR && (IL_FUSE1 || IL_LOOP2)
 #error "IL_BOUND_FLOOR is implemented for the default loop structure only"
 #endif
@@ -80,8 +100,10 @@ struct FastScalars {
     float thr2;     // diverge_threshold^2
     double dt;
     double x0_lo, x0_range;
-    U128 jump_mult, jump_add;  // PCG64 advance by half the stream
+    U128 jump_mult[4], jump_add[4];  // PCG64 advance by 1, 2, 3 quarter segments; [3]: half
     int f_mvm, n_steps;
+    int n_slots;  // problems whose G a CTA stages (IL_TMA_G)
+    int b_valid;  // anneal rows per problem that enter the selection (screened energies)
 };
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
@@ -176,8 +198,17 @@ struct FastLayout {
     static constexpr int KT = (NT + 1) / 2;               // k16 tiles of the f16 MMA
     static constexpr int kFragF4 = KT * NT * 32;          // uint4 per warp
     static constexpr int kX0F4 = (16 * S + 3) / 4;        // x0 staging, aliased
-    static constexpr int kWarpF4 = kFragF4 > kX0F4 ? kFragF4 : kX0F4;
-    static constexpr size_t kSmem = sizeof(float4) * kWarpsPerCta * kWarpF4;
+    // + one uint4 of per-warp scalars kept out of registers during the loop
+    static constexpr int kWarpF4 = (kFragF4 > kX0F4 ? kFragF4 : kX0F4) + 1;
+    static constexpr size_t kWarpBytes = sizeof(float4) * kWarpsPerCta * kWarpF4;
+    // IL_TMA_G: per staged problem G [N][N], g [N], b [N] in FP64, after the
+    // warps' fragment areas; one mbarrier per slot in front of everything
+    static constexpr bool kSmemG = IL_TMA_G && NT <= 4;
+    static constexpr size_t kSlotBytes = sizeof(double) * (N * N + 2 * N);
+    static constexpr size_t kBarBytes = 64;
+    static size_t smem(int n_slots) {
+        return kSmemG ? kBarBytes + kWarpBytes + kSlotBytes * n_slots : kWarpBytes;
+    }
 };
 
 // Tensor-core operand scaling.  The coupling product runs on f16 operands
@@ -194,7 +225,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
               const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
               FastScalars s, int8_t* __restrict__ spins, uint8_t* __restrict__ diverged,
-              double* __restrict__ energies) {
+              double* __restrict__ energies, bool screened) {
     using L = FastLayout<NT>;
     constexpr int N = L::N;
     constexpr int S = L::S;
@@ -202,33 +233,110 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     extern __shared__ __align__(16) uint4 smem_u4[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerCta + warp;
-    if (task >= n_tasks) return;
+    const bool valid = task < n_tasks;
     const int64_t prob = task / tiles_per_prob;
     const int mt = (int)(task % tiles_per_prob);
     const int B = tiles_per_prob * 16;
-    uint4* frag = smem_u4 + warp * L::kWarpF4;       // G fragments (after x0 is consumed)
-    float* x0s = reinterpret_cast<float*>(frag);      // x0 staging [16][S]
-
     const int g = lane >> 2, t = lane & 3;
     const int hown = t & 1;  // the aux spin of anneal g + 8*hown is integrated by this lane
+
+    // ---- G, g, b: FP64 copies in shared memory (TMA) or straight from global
     const double* G = Gall + prob * (int64_t)N * N;
+    const double* gv_p = gall + prob * N;
+    const double* bv_p = ball + prob * N;
+    uint4* warp_area = smem_u4;
+    uint64_t* bar = nullptr;
+    if constexpr (L::kSmemG) {
+        // slot = problem index relative to the CTA's first problem; the first
+        // warp of each slot issues its bulk copies, every warp of the slot
+        // waits on the slot's mbarrier after generating its initial states
+        uint64_t* bars = reinterpret_cast<uint64_t*>(smem_u4);
+        warp_area = smem_u4 + L::kBarBytes / sizeof(uint4);
+        const int64_t first = (int64_t)blockIdx.x * kWarpsPerCta / tiles_per_prob;
+        const int slot = (int)(prob - first);
+        char* slots = reinterpret_cast<char*>(warp_area) + L::kWarpBytes;
+        if (threadIdx.x < s.n_slots) {
+            mbar_init(bars + threadIdx.x, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (!valid) return;
+        bar = bars + slot;
+        const bool issuer = (warp == 0 || (task - 1) / tiles_per_prob != prob) && lane == 0;
+        double* Gs = reinterpret_cast<double*>(slots + L::kSlotBytes * slot);
+        if (issuer) {
+            mbar_expect_tx(bar, (uint32_t)L::kSlotBytes);
+            tma_bulk_g2s(Gs, G, sizeof(double) * N * N, bar);
+            tma_bulk_g2s(Gs + N * N, gv_p, sizeof(double) * N, bar);
+            tma_bulk_g2s(Gs + N * N + N, bv_p, sizeof(double) * N, bar);
+        }
+        G = Gs;
+        gv_p = Gs + N * N;
+        bv_p = Gs + N * N + N;
+    } else {
+        if (!valid) return;
+    }
+    uint4* frag = warp_area + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
+    float* x0s = reinterpret_cast<float*>(frag);      // x0 staging [16][S]
 
     // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
     {
         const int al = lane & 15, part = lane >> 4;
         const int a = mt * 16 + al;
+#if IL_PROBE_NO_RNG
+        for (int i = part; i < S; i += 2) x0s[al * S + i] = 0.01f * (float)((a * 7 + i * 13) % 19 - 9);
+        if (false) {
+#else
+        {
+#endif
         Pcg64 rng;
         rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)a));
+        if constexpr (IL_RNG2 && NT <= 4) {
+        // the stream is cut into 4 segments of Lseg draws; this lane runs
+        // segments 2 part and 2 part + 1 as two interleaved chains (jump-ahead)
+        constexpr int Lseg = (S + 3) / 4;
+        Pcg64 r2 = rng;
+        if (part) rng.state = add128(mul128(rng.state, s.jump_mult[1]), mul128(rng.inc, s.jump_add[1]));
+        r2.state = add128(mul128(r2.state, part ? s.jump_mult[2] : s.jump_mult[0]),
+                          mul128(r2.inc, part ? s.jump_add[2] : s.jump_add[0]));
+        const int i0 = 2 * part * Lseg;
+        float* row = x0s + al * S;
+#pragma unroll 2
+        for (int i = 0; i < Lseg; ++i) {
+            const int ia = i0 + i, ib = i0 + Lseg + i;
+            const double ua = rng.uniform(s.x0_lo, s.x0_range);
+            const double ub = r2.uniform(s.x0_lo, s.x0_range);
+            if (ia < S) row[ia] = (float)ua;
+            if (ib < S) row[ib] = (float)ub;
+        }
+        } else {
         constexpr int S0 = (S + 1) / 2;
-        if (part) rng.state = add128(mul128(rng.state, s.jump_mult), mul128(rng.inc, s.jump_add));
+        if (part) rng.state = add128(mul128(rng.state, s.jump_mult[3]), mul128(rng.inc, s.jump_add[3]));
         const int i0 = part ? S0 : 0, i1 = part ? S : S0;
         for (int i = i0; i < i1; ++i) x0s[al * S + i] = (float)rng.uniform(s.x0_lo, s.x0_range);
+        }
     }
+    }
+    if constexpr (L::kSmemG) mbar_wait(bar, 0);
 
     // ---- per-problem scale 2^sc for -K*G ------------------------------------
     const double K = s.dt * eps_p[prob];
     double gmax = 0.0;
-    for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(__ldg(G + i)));
+    if (screened) {
+        double mag = 0.0;  // sum |G| + sum |b|: the screen bound, parked in shared memory
+#pragma unroll 4
+        for (int i = lane; i < N * N; i += 32) {
+            const double v = fabs(L::kSmemG ? G[i] : __ldg(G + i));
+            gmax = fmax(gmax, v);
+            mag += v;
+        }
+        for (int i = lane; i < N; i += 32) mag += fabs(bv_p[i]);
+        mag = warp_sum(mag);
+        if (lane == 0) reinterpret_cast<double*>(frag + L::kWarpF4 - 1)[0] = mag;
+    } else {
+#pragma unroll 4
+        for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(L::kSmemG ? G[i] : __ldg(G + i)));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
     int ex = 0;
@@ -270,7 +378,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int r = 16 * kt + 2 * t + (q & 1) + 8 * (q >> 1);
-                f[q] = r < N ? (float)(-Ks * __ldg(G + r * N + c)) : 0.f;
+                f[q] = r < N ? (float)(-Ks * (L::kSmemG ? G[r * N + c] : __ldg(G + r * N + c))) : 0.f;
             }
             uint32_t h01, l01, h23, l23;
             split_h2(make_float2(f[0], f[1]), h01, l01);
@@ -283,8 +391,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
         const int i = 8 * n + 2 * t;
-        Kg[n] = make_float2((float)(Ks * gall[prob * N + i]), (float)(Ks * gall[prob * N + i + 1]));
-        nKb[n] = make_float2((float)(-Ks * ball[prob * N + i]), (float)(-Ks * ball[prob * N + i + 1]));
+        Kg[n] = make_float2((float)(Ks * gv_p[i]), (float)(Ks * gv_p[i + 1]));
+        nKb[n] = make_float2((float)(-Ks * bv_p[i]), (float)(-Ks * bv_p[i + 1]));
     }
     __syncwarp();
 
@@ -402,6 +510,30 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 }
             }
 #endif
+#if IL_FUSE_Q
+            // C-independent part of this step's Euler update (x^2, the
+            // divergence max, the x- and e-factors) in the refresh's basic
+            // block, where it can fill the tensor-core latency; the remaining
+            // operations follow the assembly below.  Same operations, same
+            // order as euler_pair: bit-identical.
+            float2 qA[2][NT], qB[2][NT];
+            [[maybe_unused]] float2 rA[2][NT], rB[2][NT];
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int n = 0; n < NT; ++n) {
+                    const float2 a2 = __fmul2_rn(xA[h][n], xA[h][n]);
+                    dv[h][n & 1] = max_nan3(dv[h][n & 1], a2.x, a2.y);
+                    qA[h][n] = __ffma2_rn(make_float2(s.ndt, s.ndt), a2, make_float2(s.alpha, s.alpha));
+                    const float2 b2 = __fmul2_rn(xB[h][n], xB[h][n]);
+                    dv[h][n & 1] = max_nan3(dv[h][n & 1], b2.x, b2.y);
+                    qB[h][n] = __ffma2_rn(make_float2(s.ndt, s.ndt), b2, make_float2(s.alpha, s.alpha));
+                    if constexpr (!SAME_QR) {
+                        rA[h][n] = __ffma2_rn(make_float2(s.ndtz, s.ndtz), a2, make_float2(s.beta, s.beta));
+                        rB[h][n] = __ffma2_rn(make_float2(s.ndtz, s.ndtz), b2, make_float2(s.beta, s.beta));
+                    }
+                }
+#endif
             // ---- coupling assembly: C_s = M' + Ks g x_self - Ks b xa ----------
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
@@ -418,9 +550,28 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                     const float2 u2 = __ffma2_rn(nKb[n], make_float2(xah, xah), m2);
                     CA[h][n] = __ffma2_rn(Kg[n], xA[h][n], u2);
                     CB[h][n] = __ffma2_rn(Kg[n], xB[h][n], u2);
+#if IL_FUSE_Q
+                    xA[h][n] = __ffma2_rn(eA[h][n], CA[h][n], __fmul2_rn(xA[h][n], qA[h][n]));
+                    xB[h][n] = __ffma2_rn(eB[h][n], CB[h][n], __fmul2_rn(xB[h][n], qB[h][n]));
+                    if constexpr (SAME_QR) {
+                        eA[h][n] = __fmul2_rn(eA[h][n], qA[h][n]);
+                        eB[h][n] = __fmul2_rn(eB[h][n], qB[h][n]);
+                    } else {
+                        eA[h][n] = __fmul2_rn(eA[h][n], rA[h][n]);
+                        eB[h][n] = __fmul2_rn(eB[h][n], rB[h][n]);
+                    }
+#if !IL_BOUND_FLOOR
+                    eA[h][n] = floor2(eA[h][n], e_floor);
+                    eB[h][n] = floor2(eB[h][n], e_floor);
+#endif
+#endif
                 }
             }
         }
+#if IL_FUSE_Q
+        else
+#endif
+        {
 #if IL_FUSE1
         // first Euler step of the period in the refresh's basic block
 #pragma unroll
@@ -446,6 +597,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, e_floor, dv[h][n & 1]);
                 euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
             }
+        }
         }
 #if IL_BOUND_FLOOR
         // e' = max(e_floor, e r).  Every e of this thread stays >= e_lb, a
@@ -489,6 +641,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     dvh[hown] = max_nan(dvh[hown], max_nan(dva, xa * xa));  // own aux spin
     const int64_t row0 = prob * (int64_t)B + mt * 16;
     uint64_t pos[2], neg[2];
+    bool dflag[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         float d = dvh[h];
@@ -518,12 +671,116 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         pos[h] = pm;
         neg[h] = nm;
         if (t == h) sp[2 * N] = xa >= 0.f ? 1 : -1;
-        if (t == 0) diverged[row] = (d <= s.thr2) ? 0 : 1;
+        dflag[h] = !(d <= s.thr2);
+        if (t == 0) diverged[row] = dflag[h] ? 1 : 0;
+    }
+    if (screened) {
+        // Selection screen: E + 2 tr G in FP32 from the tensor cores.  u =
+        // s_A + s_B in {-2, 0, 2} is exact in f16, so two passes over the
+        // staged hi/lo fragments give M = (-Ks G) u to ~2^-21 of sum|G|; the
+        // anneals that can still be the argmin are re-evaluated in FP64.
+        float2 u[2][NT];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+                u[h][n] = make_float2((xA[h][n].x >= 0.f ? 1.f : -1.f) + (xB[h][n].x >= 0.f ? 1.f : -1.f),
+                                      (xA[h][n].y >= 0.f ? 1.f : -1.f) + (xB[h][n].y >= 0.f ? 1.f : -1.f));
+        float acc[NT][4];
+#pragma unroll
+        for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+#pragma unroll
+        for (int kt = 0; kt < KT; ++kt) {
+            uint32_t a[4];
+            a[0] = h2_bits(__float22half2_rn(u[0][2 * kt]));
+            a[1] = h2_bits(__float22half2_rn(u[1][2 * kt]));
+            a[2] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[0][2 * kt + 1])) : 0u;
+            a[3] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[1][2 * kt + 1])) : 0u;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                const uint4 f = frag[(kt * NT + n) * 32 + lane];
+                mma_f16(acc[n], a, f.z, f.w);
+                mma_f16(acc[n], a, f.x, f.y);
+            }
+        }
+        // unscaled FP32-screen energies (without -2 tr G) of rows g, g+8
+        double es[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float q = 0.f, l = 0.f;
+#pragma unroll
+            for (int n = 0; n < NT; ++n) {
+                q = fmaf(u[h][n].x, acc[n][2 * h], q);
+                q = fmaf(u[h][n].y, acc[n][2 * h + 1], q);
+                l = fmaf(nKb[n].x, u[h][n].x, l);
+                l = fmaf(nKb[n].y, u[h][n].y, l);
+            }
+            float e = fmaf(xa_h[h] >= 0.f ? 2.f : -2.f, l, q);  // -Ks (u'Gu + 2 s_aux b'u)
+            e += __shfl_xor_sync(0xffffffffu, e, 1);
+            e += __shfl_xor_sync(0xffffffffu, e, 2);
+            // padded rows (>= b_valid) never enter the selection
+            es[h] = (dflag[h] || mt * 16 + g + 8 * h >= s.b_valid) ? INFINITY : (double)e * (-1.0 / Ks);
+        }
+        // tile minimum over survivors; candidates within 2 x 2^-12 mag of it
+        // (the screen error is < 2^-13 mag, see launch_anneal_fast)
+        double m = fmin(es[0], es[1]);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
+        const double lim = m + 0x1p-11 * reinterpret_cast<const double*>(frag + L::kWarpF4 - 1)[0];
+        // lane 4g + h stands for row g + 8h (h < 2)
+        const int hs = t & 1;
+        const uint64_t my_pos = pos[hs], my_neg = neg[hs];
+        const bool my_aux = xa >= 0.f;  // aux of row g + 8 hown, hown == hs
+        const bool my_cand = t < 2 && es[hs] <= lim;
+        unsigned cand = __ballot_sync(0xffffffffu, my_cand);
+        double my_e = INFINITY;
+        double* w = reinterpret_cast<double*>(frag);  // fragments are consumed
+        __syncwarp();
+        double tr = 0.0;
+        for (int i = lane; i < N; i += 32) tr += G[(int64_t)i * N + i];
+        tr = warp_sum(tr);
+        while (cand) {
+            const int l = __ffs(cand) - 1;
+            const uint64_t cp = __shfl_sync(0xffffffffu, my_pos, l);
+            const uint64_t cn = __shfl_sync(0xffffffffu, my_neg, l);
+            const bool cax = __shfl_sync(0xffffffffu, my_aux, l);
+            // E = u'Gu - 2 tr G + 2 s_aux b'u with u = 2 w (solver.py:171-175);
+            // lane i sums row i through column i of the symmetric G
+            for (int j = lane; j < N; j += 32)
+                w[j] = (double)((int)((cp >> j) & 1u) - (int)((cn >> j) & 1u));
+            __syncwarp();
+            double q = 0.0, li = 0.0;
+            for (int i = lane; i < N; i += 32) {
+                double gu[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int j = 0; j < N; j += 4)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r)
+                        gu[r] = fma(L::kSmemG ? G[(j + r) * N + i] : __ldg(G + (int64_t)(j + r) * N + i),
+                                    w[j + r], gu[r]);
+                q = fma(w[i], (gu[0] + gu[1]) + (gu[2] + gu[3]), q);
+                li = fma(bv_p[i], w[i], li);
+            }
+            __syncwarp();
+            q = warp_sum(q);
+            li = warp_sum(li);
+            const double e = (4.0 * q - 2.0 * tr) + (cax ? 4.0 : -4.0) * li;
+            // identical configurations have identical energies
+            const bool same = my_cand && my_pos == cp && my_neg == cn && my_aux == cax;
+            if (same) my_e = e;
+            cand &= ~__ballot_sync(0xffffffffu, same);
+        }
+        if (t < 2) energies[row0 + g + 8 * t] = my_e;
+        return;
     }
     // FP64 energies.  Row sums use G's symmetry: sum_j s_j G[j][i] reads row j
     // at this lane's columns i = 8n+2t+{0,1} (16-byte loads), with s_j decoded
     // once per j for both anneals.
-    const double* bg = ball + prob * N;
+    const double* bg = bv_p;
+#if IL_PROBE_NO_ENERGY
+    if (t < 2) energies[row0 + g + 8 * t] = (double)(pos[t] ^ neg[t]);
+    return;
+#endif
     double rs[2][2 * NT];
 #pragma unroll
     for (int k = 0; k < 2 * NT; ++k) rs[0][k] = rs[1][k] = 0.0;
@@ -533,7 +790,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         const double* Gj = G + (int64_t)j * N + 2 * t;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-            const double2 gv = __ldg(reinterpret_cast<const double2*>(Gj + 8 * n));
+            const double2 gv = L::kSmemG ? *reinterpret_cast<const double2*>(Gj + 8 * n)
+                                         : __ldg(reinterpret_cast<const double2*>(Gj + 8 * n));
             rs[0][2 * n] = fma(gv.x, s0, rs[0][2 * n]);
             rs[0][2 * n + 1] = fma(gv.y, s0, rs[0][2 * n + 1]);
             rs[1][2 * n] = fma(gv.x, s1, rs[1][2 * n]);
@@ -550,10 +808,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             const double si1 = (double)((int)((pos[1] >> i) & 1u) - (int)((neg[1] >> i) & 1u));
             quad[0] = fma(si0, rs[0][2 * n + dl], quad[0]);
             quad[1] = fma(si1, rs[1][2 * n + dl], quad[1]);
-            const double bi = __ldg(bg + i);
+            const double bi = bg[i];
             lin[0] = fma(bi, si0, lin[0]);
             lin[1] = fma(bi, si1, lin[1]);
-            tr += __ldg(G + (int64_t)i * N + i);
+            tr += G[(int64_t)i * N + i];
         }
     }
 #pragma unroll
@@ -574,15 +832,23 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 template <int NT, bool SPLIT, bool SAME_QR>
 int launch_cfg(const double* G, const double* g, const double* b, const uint64_t* base_seed,
                const double* eps_p, int64_t n_tasks, int tiles, const FastScalars& fs,
-               int8_t* spins, uint8_t* diverged, double* energies, cudaStream_t st) {
+               int8_t* spins, uint8_t* diverged, double* energies, bool screened,
+               cudaStream_t st) {
     const int64_t blocks = (n_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
     IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
-    const size_t smem = FastLayout<NT>::kSmem;
+    // distinct problems per CTA (periodic in the block index, period <= tiles)
+    FastScalars f2 = fs;
+    f2.n_slots = 1;
+    for (int64_t blk = 0; blk < std::min<int64_t>(blocks, tiles); ++blk) {
+        const int64_t t0 = blk * kWarpsPerCta, t1 = std::min(n_tasks, t0 + kWarpsPerCta) - 1;
+        f2.n_slots = std::max<int>(f2.n_slots, (int)(t1 / tiles - t0 / tiles + 1));
+    }
+    const size_t smem = FastLayout<NT>::smem(f2.n_slots);
     auto fn = k_anneal_fast<NT, SPLIT, SAME_QR>;
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     IL_LAUNCH(kProfAnneal, st, fn<<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(G, g, b, base_seed, eps_p, n_tasks, tiles,
-                                                        fs, spins, diverged, energies););
+                                                        f2, spins, diverged, energies, screened););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -590,19 +856,20 @@ int launch_cfg(const double* G, const double* g, const double* b, const uint64_t
 template <int NT>
 int launch_nt(const double* G, const double* g, const double* b, const uint64_t* base_seed,
               const double* eps_p, int64_t P, int B, const FastScalars& fs, bool split,
-              bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, cudaStream_t st) {
+              bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, bool screened,
+              cudaStream_t st) {
     const int tiles = B / 16;
     const int64_t n_tasks = P * tiles;
     if (split) {
         return same_qr ? launch_cfg<NT, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                   spins, diverged, energies, st)
+                                                   spins, diverged, energies, screened, st)
                        : launch_cfg<NT, true, false>(G, g, b, base_seed, eps_p, n_tasks, tiles,
-                                                    fs, spins, diverged, energies, st);
+                                                    fs, spins, diverged, energies, screened, st);
     }
     return same_qr ? launch_cfg<NT, false, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                spins, diverged, energies, st)
+                                                spins, diverged, energies, screened, st)
                    : launch_cfg<NT, false, false>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                 spins, diverged, energies, st);
+                                                 spins, diverged, energies, screened, st);
 }
 
 // PCG64 advance-by-k constants: state_k = M^k state_0 + inc * (M^{k-1} + ... + 1)
@@ -635,7 +902,7 @@ bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st) {
+                       double* energies, cudaStream_t st, int screen_rows) {
     if (!fast_anneal_supported(N, B, s)) {
         set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
         return IL_ERR_UNSUPPORTED;
@@ -653,13 +920,17 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.x0_range = s.x0_range;
     fs.f_mvm = s.f_mvm;
     fs.n_steps = s.n_steps;
-    pcg_jump((2 * N + 2) / 2, &fs.jump_mult, &fs.jump_add);
+    fs.b_valid = screen_rows;
+    // the screen pays off from N = 24 on (at N = 16 the FP64 epilogue is cheaper)
+    const bool screened = screen_rows > 0 && N >= 24;
+    for (int k = 0; k < 3; ++k) pcg_jump((k + 1) * ((2 * N + 1 + 3) / 4), &fs.jump_mult[k], &fs.jump_add[k]);
+    pcg_jump((2 * N + 2) / 2, &fs.jump_mult[3], &fs.jump_add[3]);
     const bool split = precision != IL_PREC_TF32;
     // x and e share their per-step factor exactly when zeta*dt == dt and
     // 1 + dt (p - 1) == 1 + dt zeta a in FP32 (the reference defaults)
     const bool same_qr = fs.alpha == fs.beta && fs.ndt == fs.ndtz;
 #define IL_NT(k) \
-    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, st)
+    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, st)
     switch (N / 8) {
         IL_NT(1);
         IL_NT(2);

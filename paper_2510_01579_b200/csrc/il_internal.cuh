@@ -24,10 +24,16 @@ int launch_anneal_exact(const double* G, const double* g, const double* b, const
 // B % 16 == 0.  Divergence is a sticky flag (spins of diverged anneals are
 // not frozen: they never enter selection).  Returns IL_ERR_UNSUPPORTED when
 // the shape is not instantiated.
+// Energies: the FP64 energy of every anneal; or, with screen_rows > 0, only of
+// the anneals among the first screen_rows rows of each problem that can be the
+// FP64 argmin of those rows (+inf for the others):
+// an FP32 tensor-core screen bounds every energy to within 2^-13 (sum|G| +
+// sum|b|) and only the distinct configurations within twice that of the
+// minimum are evaluated in FP64.  The argmin (ties -> lowest row) is the same.
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st);
+                       double* energies, cudaStream_t st, int screen_rows = 0);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
 // anneal rows per problem the fast kernel runs for B requested anneals
 inline int fast_rows(int B) { return (B + 15) / 16 * 16; }
@@ -157,6 +163,11 @@ struct Workspace {
     template <class T>
     T* get(size_t count, int* rc) {
         if (*rc != IL_OK) return nullptr;
+        if (n >= 32) {
+            set_error("workspace: too many buffers");
+            *rc = IL_ERR_CUDA;
+            return nullptr;
+        }
         void* p = nullptr;
         cudaError_t e = cudaMallocAsync(&p, count ? count * sizeof(T) : 1, st);
         if (e != cudaSuccess) {
