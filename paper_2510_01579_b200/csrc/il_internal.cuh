@@ -35,6 +35,13 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
                        double* energies, cudaStream_t st, int screen_rows = 0);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
+// The same anneal with the coupling product on tcgen05 (anneal_umma.cu);
+// launch_anneal_fast dispatches to it when enabled and supported.
+bool umma_anneal_supported(int N, int B);
+int launch_anneal_umma(const double* G, const double* g, const double* b,
+                       const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
+                       const void* fast_scalars, bool split, bool same_qr, int8_t* spins,
+                       uint8_t* diverged, double* energies, bool screened, cudaStream_t st);
 // anneal rows per problem the fast kernel runs for B requested anneals
 inline int fast_rows(int B) { return (B + 15) / 16 * 16; }
 
