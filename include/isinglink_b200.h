@@ -157,6 +157,15 @@ int il_integrate_batch(const double* G, const double* g_diag, const double* b,
 int il_ml_batch(const double* H, const double* y, int64_t P, int32_t n_r, int32_t n_t,
                 int32_t qam_order, uint8_t* x_idx, double* energy, void* stream);
 
+/* Max-log bit LLRs by the same exhaustive search (n_r <= 16, <= 24 bits).
+ * No reference counterpart (soft output is a non-goal of the reference,
+ * SPEC.md:153; parity unpinned): llr[P * n_t * 2 * bits_per_dim] with bits in
+ * the order of il_gray_demap (user, re then im, MSB first) and
+ *   llr = (min_{x: bit = 1} ||y - Hx||^2 - min_{x: bit = 0} ||y - Hx||^2) / s2,
+ * s2 = noise_var[p] (1 when noise_var is NULL): positive favours bit 0. */
+int il_ml_llr_batch(const double* H, const double* y, const double* noise_var, int64_t P,
+                    int32_t n_r, int32_t n_t, int32_t qam_order, double* llr, void* stream);
+
 /* ---------------------------------------------------------------------------
  * Batched uplink detection: P x detect_cim (detector.py:57-82) with
  * seed[p] the `seed` argument of detect_cim for problem p.  Outputs:

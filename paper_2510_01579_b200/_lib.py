@@ -51,6 +51,7 @@ _SIGS = {
                             ctypes.c_int),
     "il_residual_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _vp, _vp], ctypes.c_int),
     "il_ml_batch": ([_vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp], ctypes.c_int),
+    "il_ml_llr_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp], ctypes.c_int),
     "il_integrate_batch": ([_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32, ctypes.POINTER(CacParamsC),
                             _vp, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "il_mmse_sic_batch": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp, _vp, _vp, _vp],

@@ -180,6 +180,21 @@ def detect_ml(inst: MimoInstance) -> DetectionResult:
     return DetectionResult(x_hard=x, energy=float(energy[0]), source="ml")
 
 
+def ml_llr(inst: MimoInstance) -> np.ndarray:
+    """Max-log bit LLRs of the exhaustive search, [n_t, bits_per_symbol] in
+    the Gray-demapper bit order, (d1 - d0) / noise_var: positive favours bit 0.
+    No reference counterpart (soft output is a reference non-goal,
+    SPEC.md:153); the sign agrees with the bits of ``detect_ml``."""
+    bits = inst.n_t * inst.constellation.bits_per_symbol
+    if bits > ML_MAX_BITS:
+        raise ValueError(f"ML search space of {bits} bits exceeds the {ML_MAX_BITS}-bit guard")
+    if inst.H.shape[0] > 16:
+        raise ValueError("ml_llr supports n_r <= 16")
+    llr = batched.ml_llr_batch(inst.H[None], inst.y[None], _order_code(inst.constellation),
+                               noise_var=[float(inst.noise_var)])
+    return llr[0].cpu().numpy()
+
+
 def build_ising(inst: MimoInstance, x_guess: np.ndarray) -> StructuredIsing:
     """transform.py:108-140 on the GPU, around a constellation-point guess."""
     x_guess = np.asarray(x_guess, dtype=complex)

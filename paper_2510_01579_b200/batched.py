@@ -13,6 +13,7 @@ reference-shaped per-instance API in ``api.py`` is built on them.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -233,6 +234,23 @@ def ml_batch(H, y, order: int):
     _lib.call("il_ml_batch", Hd.data_ptr(), yd.data_ptr(), P, n_r, n_t, int(order),
               x_idx.data_ptr(), energy.data_ptr(), _stream())
     return x_idx, energy
+
+
+def ml_llr_batch(H, y, order: int, noise_var=None) -> torch.Tensor:
+    """Max-log bit LLRs by exhaustive search -> [P, n_t, 2 * bits_per_dim]
+    (bit order of ``gray_demap``; positive favours bit 0).  No reference
+    counterpart: soft output is a non-goal of the reference."""
+    Hd = _dev(H, torch.complex128)
+    P, n_r, n_t = Hd.shape
+    yd = _dev(y, torch.complex128)
+    m = int(round(math.sqrt(order)))
+    bpd = max(1, int(round(math.log2(m))))
+    nv = None if noise_var is None else _dev(torch.as_tensor(noise_var, dtype=torch.float64)
+                                              .reshape(-1).expand(P).contiguous(), torch.float64)
+    llr = torch.empty((P, n_t, 2 * bpd), dtype=torch.float64, device=Hd.device)
+    _lib.call("il_ml_llr_batch", Hd.data_ptr(), yd.data_ptr(), 0 if nv is None else nv.data_ptr(),
+              P, n_r, n_t, int(order), llr.data_ptr(), _stream())
+    return llr
 
 
 def integrate_batch(G, g_diag, b, eps, seeds, params=None) -> dict:

@@ -319,6 +319,16 @@ int il_ml_batch(const double* H, const double* y, int64_t P, int32_t n_r, int32_
     return launch_ml(H, y, P, n_r, n_t, al, x_idx, energy, (cudaStream_t)stream);
 }
 
+int il_ml_llr_batch(const double* H, const double* y, const double* noise_var, int64_t P,
+                    int32_t n_r, int32_t n_t, int32_t qam_order, double* llr, void* stream) {
+    IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= 1, "invalid shape");
+    IL_REQUIRE(P == 0 || (H && y && llr), "NULL buffer");
+    Alphabet al;
+    int rc = make_qam_alphabet(qam_order, &al);
+    if (rc) return rc;
+    return launch_ml_llr(H, y, noise_var, P, n_r, n_t, al, llr, (cudaStream_t)stream);
+}
+
 int il_mmse_sic_batch(const double* H, const double* y, const double* noise_var, int64_t P,
                       int32_t n_r, int32_t n_t, int32_t qam_order, uint8_t* x_idx, double* energy,
                       int8_t* status, void* stream) {

@@ -100,6 +100,8 @@ int launch_multi_stage(const int32_t* stage_ai, int64_t P, int32_t* widx, cudaSt
 int launch_multi_combine(const uint8_t* gx, const double* ge, const int32_t* widx, int64_t P,
                          int nx, uint8_t* x, double* e, int8_t* src, int32_t* aidx,
                          cudaStream_t st);
+int launch_ml_llr(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
+                  int n_t, const Alphabet& al, double* llr, cudaStream_t st);
 int launch_ml(const double* H, const double* y, int64_t P, int n_r, int n_t, const Alphabet& al,
               uint8_t* x_idx, double* energy, cudaStream_t st);
 int launch_spin_energies(const double* G, const double* b, const int8_t* spins, int64_t P, int B,

@@ -125,6 +125,125 @@ k_ml(const double* __restrict__ Hg, const double* __restrict__ yg, int64_t P, in
     }
 }
 
+// Max-log bit LLRs by the same exhaustive search (no reference: soft output is
+// a non-goal of the reference, SPEC.md:153 -- the definition is the standard
+// max-log one and is pinned only against the oracle's brute force):
+//   LLR_b = (min_{x: b(x) = 1} ||y - Hx||^2 - min_{x: b(x) = 0} ||y - Hx||^2) / s2
+// with bit b = (user j, re/im, Gray bit q MSB first) in the order of the Gray
+// demapper (channel.py:160-180), so LLR_b > 0 favours bit 0.  A thread keeps
+// the minima of the last user's bits per candidate and those of the prefix
+// users once per prefix (the minimum over its M completions).
+constexpr int kLlrMaxBits = 24, kLlrMaxLast = 16, kLlrMaxNr = 16;
+
+__global__ void __launch_bounds__(kMlThreads)
+k_ml_llr(const double* __restrict__ Hg, const double* __restrict__ yg,
+         const double* __restrict__ noise_var, int64_t P, int n_r, int n_t, Alphabet al,
+         int64_t n_prefix, int bpd, double* __restrict__ llr) {
+    extern __shared__ __align__(16) cplx sm[];
+    const int64_t prob = blockIdx.x;
+    if (prob >= P) return;
+    const int m = al.m, M = m * m, nb = 2 * bpd * n_t, nl = 2 * bpd, npre = nb - nl;
+    cplx* H = sm;
+    cplx* y = H + n_r * n_t;
+    cplx* pts = y + n_r;
+    __shared__ double red[2][kMlThreads / 32][kLlrMaxBits];
+    const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n_t;
+    for (int i = threadIdx.x; i < n_r * n_t; i += kMlThreads) H[i] = Hp[i];
+    for (int i = threadIdx.x; i < n_r; i += kMlThreads)
+        y[i] = reinterpret_cast<const cplx*>(yg)[prob * n_r + i];
+    for (int d = threadIdx.x; d < M; d += kMlThreads) pts[d] = {al.levels[d / m], al.levels[d % m]};
+    __syncthreads();
+
+    // Gray bits of symbol d as one 2 bpd-bit word: re label (high bits) then
+    // im label, bit q of the symbol (MSB first) at 2 bpd - 1 - q
+    auto sym_bits = [&](int d) -> int {
+        const int ire = d / m, iim = d - ire * m;
+        return ((ire ^ (ire >> 1)) << bpd) | (iim ^ (iim >> 1));
+    };
+    double mpre[2][kLlrMaxBits], mlast[2][kLlrMaxLast];
+#pragma unroll
+    for (int b = 0; b < kLlrMaxBits; ++b) mpre[0][b] = mpre[1][b] = INFINITY;
+#pragma unroll
+    for (int b = 0; b < kLlrMaxLast; ++b) mlast[0][b] = mlast[1][b] = INFINITY;
+    cplx r[kLlrMaxNr];
+    const int last = n_t - 1;
+    for (int64_t pfx = threadIdx.x; pfx < n_prefix; pfx += kMlThreads) {
+#pragma unroll
+        for (int i = 0; i < kLlrMaxNr; ++i)
+            if (i < n_r) r[i] = y[i];
+        int64_t div = n_prefix;
+        for (int j = 0; j < last; ++j) {
+            div /= M;
+            const cplx x = pts[(pfx / div) % M];
+#pragma unroll
+            for (int i = 0; i < kLlrMaxNr; ++i)
+                if (i < n_r) r[i] = sub_mul(r[i], H[i * n_t + j], x);
+        }
+        double emin = INFINITY;
+        for (int d = 0; d < M; ++d) {
+            const cplx x = pts[d];
+            double e = 0.0;
+#pragma unroll
+            for (int i = 0; i < kLlrMaxNr; ++i) {
+                if (i < n_r) {
+                    const cplx ri = sub_mul(r[i], H[i * n_t + last], x);
+                    e = __dadd_rn(e, __fma_rn(ri.re, ri.re, __dmul_rn(ri.im, ri.im)));
+                }
+            }
+            emin = fmin(emin, e);
+            const int word = sym_bits(d);
+#pragma unroll
+            for (int q = 0; q < kLlrMaxLast; ++q) {
+                if (q < nl) {
+                    const int bit = (word >> (nl - 1 - q)) & 1;
+                    mlast[0][q] = bit ? mlast[0][q] : fmin(mlast[0][q], e);
+                    mlast[1][q] = bit ? fmin(mlast[1][q], e) : mlast[1][q];
+                }
+            }
+        }
+        // prefix users: the best completion of this prefix
+#pragma unroll
+        for (int b = 0; b < kLlrMaxBits; ++b) {
+            if (b < npre) {
+                const int j = b / nl, q = b % nl;
+                int64_t dv = n_prefix;
+                for (int k = 0; k <= j; ++k) dv /= M;
+                const int bit = (sym_bits((int)((pfx / dv) % M)) >> (nl - 1 - q)) & 1;
+                mpre[0][b] = bit ? mpre[0][b] : fmin(mpre[0][b], emin);
+                mpre[1][b] = bit ? fmin(mpre[1][b], emin) : mpre[1][b];
+            }
+        }
+    }
+    // block minima per (bit value, position)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+#pragma unroll
+        for (int b = 0; b < kLlrMaxBits; ++b) {
+            double x = b < npre ? mpre[v][b] : INFINITY;
+            if (b >= npre && b - npre < kLlrMaxLast) {
+#pragma unroll
+                for (int q = 0; q < kLlrMaxLast; ++q)
+                    if (q == b - npre) x = mlast[v][q];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) x = fmin(x, __shfl_xor_sync(0xffffffffu, x, o));
+            if (lane == 0) red[v][warp][b] = x;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < nb) {
+        const int b = threadIdx.x;
+        double d0 = INFINITY, d1 = INFINITY;
+        for (int w = 0; w < kMlThreads / 32; ++w) {
+            d0 = fmin(d0, red[0][w][b]);
+            d1 = fmin(d1, red[1][w][b]);
+        }
+        const double s2 = noise_var ? noise_var[prob] : 1.0;
+        llr[prob * nb + b] = (d1 - d0) / s2;
+    }
+}
+
 }  // namespace
 
 int launch_ml(const double* H, const double* y, int64_t P, int n_r, int n_t, const Alphabet& al,
@@ -148,4 +267,27 @@ int launch_ml(const double* H, const double* y, int64_t P, int n_r, int n_t, con
     return IL_OK;
 }
 
+}  // namespace il
+
+namespace il {
+int launch_ml_llr(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
+                  int n_t, const Alphabet& al, double* llr, cudaStream_t st) {
+    if (P == 0) return IL_OK;
+    IL_REQUIRE(n_r <= kLlrMaxNr, "ML LLRs support n_r <= %d", kLlrMaxNr);
+    const int M = al.m * al.m;
+    int bpd = 0;
+    while ((1 << bpd) < al.m) ++bpd;
+    IL_REQUIRE(2 * bpd * n_t <= kLlrMaxBits && 2 * bpd <= kLlrMaxLast,
+               "ML search space of %d bits exceeds the 24-bit guard", 2 * bpd * n_t);
+    int64_t n_prefix = 1;
+    for (int j = 0; j < n_t - 1; ++j) n_prefix *= M;
+    const size_t smem = sizeof(cplx) * ((size_t)n_r * n_t + n_r + M);
+    IL_CHECK_CUDA(cudaFuncSetAttribute(k_ml_llr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    IL_REQUIRE(P < (1ll << 31), "too many problems");
+    IL_LAUNCH(kProfOther, st,
+              k_ml_llr<<<(unsigned)P, kMlThreads, smem, st>>>(H, y, noise_var, P, n_r, n_t, al,
+                                                              n_prefix, bpd, llr););
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
 }  // namespace il

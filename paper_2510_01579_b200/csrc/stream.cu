@@ -10,6 +10,7 @@
 // required for the overlap (pageable memory works but the copies then
 // serialise with the host thread; pageable outputs only delay the tail).
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -20,6 +21,9 @@ using namespace il;
 #ifndef IL_PIPE_CAP_DIV
 #define IL_PIPE_CAP_DIV 16
 #endif
+#ifndef IL_PIPE_FIRST_DIV
+#define IL_PIPE_FIRST_DIV 48
+#endif
 
 namespace {
 
@@ -27,12 +31,16 @@ namespace {
 // creating 4 streams and 2 x n_chunks events per call cost ~0.4 ms.  Calls
 // are serialised by the mutex (the pipeline owns its streams for the call).
 struct Streams {
-    cudaStream_t in = nullptr, out = nullptr, comp[2] = {nullptr, nullptr};
+    static constexpr int kMaxComp = 4;
+    cudaStream_t in = nullptr, out = nullptr, comp[kMaxComp] = {};
     std::vector<cudaEvent_t> ev;
     int init(int n_events) {
         if (!in)
-            for (cudaStream_t* s : {&in, &out, &comp[0], &comp[1]})
+        {
+            for (cudaStream_t* s : {&in, &out})
                 IL_CHECK_CUDA(cudaStreamCreateWithFlags(s, cudaStreamNonBlocking));
+            for (cudaStream_t& s : comp) IL_CHECK_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        }
         while ((int)ev.size() < n_events) {
             cudaEvent_t e;
             IL_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -65,10 +73,19 @@ struct PipeBuf {
     char* dev = nullptr;
 };
 
+// ISINGLINK_PIPE_{FIRST,CAP}_DIV override the ramp (tuning runs)
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    const int v = e && *e ? atoi(e) : 0;
+    return v > 0 ? v : dflt;
+}
+
 // Chunk boundaries: n_chunks > 0 -> equal chunks; otherwise (P >= 4096) a
 // ramp: a small first chunk (~P/48, its H2D is the exposed latency) doubling
 // up to P/16, so few chunks carry wave tails.
 std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
+    static const int cap_div = env_int("ISINGLINK_PIPE_CAP_DIV", IL_PIPE_CAP_DIV);
+    static const int first_div = env_int("ISINGLINK_PIPE_FIRST_DIV", IL_PIPE_FIRST_DIV);
     std::vector<int64_t> bounds{0};
     if (n_chunks > 0 || P < 4096) {
         if (n_chunks <= 0) n_chunks = 1;
@@ -77,8 +94,8 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
         chunk = (chunk + 7) / 8 * 8;
         while (bounds.back() < P) bounds.push_back(std::min(P, bounds.back() + chunk));
     } else {
-        const int64_t cap = std::max<int64_t>(P / IL_PIPE_CAP_DIV, 8);
-        int64_t c = std::max<int64_t>(P / 48, 256);
+        const int64_t cap = std::max<int64_t>(P / cap_div, 8);
+        int64_t c = std::max<int64_t>(P / first_div, 256);
         while (bounds.back() < P) {
             const int64_t cc = (std::min(c, cap) + 7) / 8 * 8;
             bounds.push_back(std::min(P, bounds.back() + cc));
@@ -102,7 +119,8 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
     IL_REQUIRE(dev_id < 64, "device ordinal out of range");
     std::lock_guard<std::mutex> lock(g_pipe_mu);
     Streams& ss = g_pipe[dev_id];
-    int rc = ss.init(2 * K + 1);
+    static const int n_comp = std::min(Streams::kMaxComp, env_int("ISINGLINK_PIPE_STREAMS", 2));
+    int rc = ss.init(std::max(2 * K + 1, n_comp));
     if (rc) return rc;
     for (PipeBuf& b : bufs) {  // stream-ordered on `in`, published by the first event
         if (rc) break;
@@ -112,8 +130,7 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
     if (rc == IL_OK) {
         cudaEvent_t ready = ss.ev[2 * K];
         cudaEventRecord(ready, ss.in);
-        cudaStreamWaitEvent(ss.comp[0], ready, 0);
-        cudaStreamWaitEvent(ss.comp[1], ready, 0);
+        for (int k = 0; k < n_comp; ++k) cudaStreamWaitEvent(ss.comp[k], ready, 0);
         cudaStreamWaitEvent(ss.out, ready, 0);
         for (int c = 0; c < K && rc == IL_OK; ++c) {
             const int64_t o = bounds[c], n = bounds[c + 1] - o;
@@ -122,7 +139,7 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
                     cudaMemcpyAsync(b.dev + o * b.bytes, (const char*)b.host_in + o * b.bytes,
                                     n * b.bytes, cudaMemcpyHostToDevice, ss.in);
             cudaEventRecord(ss.ev[2 * c], ss.in);
-            cudaStream_t cs = ss.comp[c & 1];
+            cudaStream_t cs = ss.comp[c % n_comp];
             cudaStreamWaitEvent(cs, ss.ev[2 * c], 0);
             rc = compute(o, n, cs);
             if (rc) break;
@@ -138,10 +155,10 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
         }
     }
     // frees are ordered after every use: join the compute streams into `out`
-    cudaEventRecord(ss.ev[0], ss.comp[0]);
-    cudaEventRecord(ss.ev[1], ss.comp[1]);
-    cudaStreamWaitEvent(ss.out, ss.ev[0], 0);
-    cudaStreamWaitEvent(ss.out, ss.ev[1], 0);
+    for (int k = 0; k < n_comp; ++k) {
+        cudaEventRecord(ss.ev[k], ss.comp[k]);
+        cudaStreamWaitEvent(ss.out, ss.ev[k], 0);
+    }
     for (PipeBuf& b : bufs)
         if (b.dev) cudaFreeAsync(b.dev, ss.out);
     cudaError_t e = cudaStreamSynchronize(ss.out);
