@@ -819,7 +819,12 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.n_steps = s.n_steps;
     fs.b_valid = screen_rows;
     // the screen pays off from N = 24 on (at N = 16 the FP64 epilogue is cheaper)
-    const bool screened = screen_rows > 0 && N >= 24;
+    // ISINGLINK_SCREEN=0 turns the screen off (the parity test compares both)
+    static const bool screen_on = [] {
+        const char* e = getenv("ISINGLINK_SCREEN");
+        return !(e && *e == '0');
+    }();
+    const bool screened = screen_on && screen_rows > 0 && N >= 24;
     for (int k = 0; k < 3; ++k) pcg_jump((k + 1) * ((2 * N + 1 + 3) / 4), &fs.jump_mult[k], &fs.jump_add[k]);
     pcg_jump((2 * N + 2) / 2, &fs.jump_mult[3], &fs.jump_add[3]);
     const bool split = precision != IL_PREC_TF32;
