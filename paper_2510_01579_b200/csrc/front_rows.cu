@@ -35,6 +35,9 @@ constexpr int kGramUnroll = IL_GRAM_UNROLL;
 #ifndef IL_PROBE_NO_LAMBDA
 #define IL_PROBE_NO_LAMBDA 0
 #endif
+#ifndef IL_FRONT_SAVE_A  // phase 1 reloads the Gram rows instead of recomputing them
+#define IL_FRONT_SAVE_A 1
+#endif
 
 // Per-group shared-memory slice (cplx units).
 IL_HD size_t rows_group_cplx(int n_r, int n, int GS) {
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kRowsThreads, IL_ROWS_MINB)
 k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
              const double* __restrict__ s2g, int64_t P, int n_r, int n, Alphabet al,
              uint8_t* __restrict__ x_idx, double* __restrict__ energy,
-             int8_t* __restrict__ status, IsingOut o) {
+             int8_t* __restrict__ status, IsingOut o, cplx* __restrict__ ascratch) {
     extern __shared__ __align__(16) cplx smem_c[];
     const Grp<GS> g;
     const int r = g.r;
@@ -252,10 +255,23 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
     double tr = 0.0;
     // phase 0 (Ising): Gram -> G, g, tr G, lambda_max;  phase 1 (MMSE): Gram -> solve.
     // One rolled loop keeps a single copy of the Gram code.
+    // with both phases, the Gram rows of phase 0 (destroyed by lambda_max)
+    // are parked in global scratch, [prob][j][r] so that a store or load of
+    // one column is 16 consecutive lanes, and phase 1 reloads them
+    cplx* asv = (DO_MMSE && DO_ISING && ascratch) ? ascratch + prob * (int64_t)GS * GS + r : nullptr;
+    cplx zr;
 #pragma unroll 1
     for (int phase = DO_ISING ? 0 : 1; phase < (DO_MMSE ? 2 : 1); ++phase) {
-        cplx zr;
-        gram_row<GS>(H, y, n_r, n, r, A, &zr);
+        if (phase == 1 && asv) {
+#pragma unroll
+            for (int j = 0; j < GS; ++j) A[j] = asv[j * GS];
+        } else {
+            gram_row<GS>(H, y, n_r, n, r, A, &zr);
+            if (phase == 0 && asv) {
+#pragma unroll
+                for (int j = 0; j < GS; ++j) asv[j * GS] = A[j];
+            }
+        }
         if (phase == 0) {
             // G rows r and n + r (16-byte stores), g_diag, trace
             if (r < n) {
@@ -401,8 +417,13 @@ int launch_rows_gs(const double* H, const double* y, const double* s2, int64_t P
     auto fn = k_front_rows<GS, M, I>;
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (P + groups - 1) / groups;
-    IL_LAUNCH(kProfFront, st, fn<<<(unsigned)blocks, kRowsThreads, smem, st>>>(H, y, s2, P, n_r, n, al, x_idx, energy, status, o););
-    IL_CHECK_CUDA(cudaGetLastError());
+    cplx* scratch = nullptr;
+    if (M && I && IL_FRONT_SAVE_A)
+        IL_CHECK_CUDA(cudaMallocAsync((void**)&scratch, sizeof(cplx) * GS * GS * (size_t)P, st));
+    IL_LAUNCH(kProfFront, st, fn<<<(unsigned)blocks, kRowsThreads, smem, st>>>(H, y, s2, P, n_r, n, al, x_idx, energy, status, o, scratch););
+    const cudaError_t e = cudaGetLastError();
+    if (scratch) cudaFreeAsync(scratch, st);
+    IL_CHECK_CUDA(e);
     return IL_OK;
 }
 
