@@ -10,6 +10,8 @@
 // required for the overlap (pageable memory works but the copies then
 // serialise with the host thread; pageable outputs only delay the tail).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -20,6 +22,9 @@ using namespace il;
 
 #ifndef IL_PIPE_CAP_DIV
 #define IL_PIPE_CAP_DIV 16
+#endif
+#ifndef IL_PIPE_TAPER  // halve the last chunks (env ISINGLINK_PIPE_TAPER=2 on, 1 off)
+#define IL_PIPE_TAPER 0
 #endif
 #ifndef IL_PIPE_FIRST_DIV
 #define IL_PIPE_FIRST_DIV 48
@@ -86,6 +91,7 @@ int env_int(const char* name, int dflt) {
 std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
     static const int cap_div = env_int("ISINGLINK_PIPE_CAP_DIV", IL_PIPE_CAP_DIV);
     static const int first_div = env_int("ISINGLINK_PIPE_FIRST_DIV", IL_PIPE_FIRST_DIV);
+    static const bool taper = env_int("ISINGLINK_PIPE_TAPER", IL_PIPE_TAPER + 1) > 1;
     std::vector<int64_t> bounds{0};
     if (n_chunks > 0 || P < 4096) {
         if (n_chunks <= 0) n_chunks = 1;
@@ -97,7 +103,11 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
         const int64_t cap = std::max<int64_t>(P / cap_div, 8);
         int64_t c = std::max<int64_t>(P / first_div, 256);
         while (bounds.back() < P) {
-            const int64_t cc = (std::min(c, cap) + 7) / 8 * 8;
+            int64_t cc = (std::min(c, cap) + 7) / 8 * 8;
+            // taper: the last chunks halve (its anneal tail has no next
+            // chunk to overlap with)
+            const int64_t rem = P - bounds.back();
+            if (taper && rem <= 2 * cap && rem > 512) cc = std::min(cc, (rem / 2 + 7) / 8 * 8);
             bounds.push_back(std::min(P, bounds.back() + cc));
             c *= 2;
         }
@@ -112,6 +122,8 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
 template <class F>
 int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& compute) {
     keep_pool_warm();
+    static const bool trace = env_int("ISINGLINK_PIPE_TRACE", 0) > 0;
+    const auto t_start = std::chrono::steady_clock::now();
     const std::vector<int64_t> bounds = chunk_bounds(P, n_chunks);
     const int K = (int)bounds.size() - 1;
     int dev_id = 0;
@@ -161,7 +173,14 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
     }
     for (PipeBuf& b : bufs)
         if (b.dev) cudaFreeAsync(b.dev, ss.out);
+    const auto t_enq = std::chrono::steady_clock::now();
     cudaError_t e = cudaStreamSynchronize(ss.out);
+    if (trace) {
+        const auto t_end = std::chrono::steady_clock::now();
+        auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+        fprintf(stderr, "[pipe] P=%lld chunks=%d enqueue %.1f us, total %.1f us\n", (long long)P, K,
+                us(t_start, t_enq), us(t_start, t_end));
+    }
     if (rc == IL_OK && e != cudaSuccess) rc = fail_cuda(e, "host pipeline");
     return rc;
 }

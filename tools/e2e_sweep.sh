@@ -1,5 +1,5 @@
 # e2e ramp sweep (dev tool, run under gpurun): host pipeline time per slot
-for f in 24 48 96; do for c in 8 12 16 24; do
+for f in ${FIRSTS:-24 48 96}; do for c in ${CAPS:-8 12 16 24}; do
   ISINGLINK_PIPE_FIRST_DIV=$f ISINGLINK_PIPE_CAP_DIV=$c python - <<'PY' 2>&1 | grep -v Warn
 import os, sys, time, torch
 sys.path.insert(0, '.')
