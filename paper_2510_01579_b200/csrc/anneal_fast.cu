@@ -72,6 +72,9 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_RNG2  // two interleaved PCG64 chains per lane for the initial states
 #define IL_RNG2 0  // measured 1% slower: the RNG is issue-bound, not latency-bound
 #endif
+#ifndef IL_KG_SMEM  // refresh constants Kg, -Kb in shared memory (frees 4 NT registers)
+#define IL_KG_SMEM 1
+#endif
 #ifndef IL_FUSE_Q  // C-independent half of the first Euler step inside the refresh block
 #define IL_FUSE_Q 0  // measured 1.4% slower (register pressure; bit-identical)
 #endif
@@ -96,7 +99,9 @@ struct FastLayout {
     static constexpr int kFragF4 = KT * NT * 32;          // uint4 per warp
     static constexpr int kX0F4 = (16 * S + 3) / 4;        // x0 staging, aliased
     // + one uint4 of per-warp scalars kept out of registers during the loop
-    static constexpr int kWarpF4 = (kFragF4 > kX0F4 ? kFragF4 : kX0F4) + 1;
+    // (IL_KG_SMEM) + NT x 32 uint4 of per-lane refresh constants {Kg, -Kb}
+    static constexpr int kKgF4 = (kFragF4 > kX0F4 ? kFragF4 : kX0F4) + 1;
+    static constexpr int kWarpF4 = kKgF4 + (IL_KG_SMEM ? NT * 32 : 0);
     static constexpr size_t kWarpBytes = sizeof(float4) * kWarpsPerCta * kWarpF4;
     // IL_TMA_G: per staged problem G [N][N], g [N], b [N] in FP64, after the
     // warps' fragment areas; one mbarrier per slot in front of everything
@@ -229,7 +234,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         }
         for (int i = lane; i < N; i += 32) mag += fabs(bv_p[i]);
         mag = warp_sum(mag);
-        if (lane == 0) reinterpret_cast<double*>(frag + L::kWarpF4 - 1)[0] = mag;
+        if (lane == 0) reinterpret_cast<double*>(frag + L::kKgF4 - 1)[0] = mag;
     } else {
 #pragma unroll 4
         for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(L::kSmemG ? G[i] : __ldg(G + i)));
@@ -284,6 +289,27 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         }
     }
     // per-thread spin constants: Ks g_i and -Ks b_i for spins 8n+2t+{0,1}
+#if IL_KG_SMEM
+    // kept in shared memory and re-read at every refresh: the registers go to
+    // the Euler update's scheduling instead
+    float4* kgs = reinterpret_cast<float4*>(frag + L::kKgF4);
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+        const int i = 8 * n + 2 * t;
+        kgs[n * 32 + lane] = make_float4((float)(Ks * gv_p[i]), (float)(Ks * gv_p[i + 1]),
+                                         (float)(-Ks * bv_p[i]), (float)(-Ks * bv_p[i + 1]));
+    }
+    auto kg_ld = [&](int n) {
+        float4 r;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "r"(smem_u32(kgs + n * 32 + lane)));
+        return r;
+    };
+    auto kg4 = [&](int n) { return kg_ld(n); };
+#define IL_KG(n) ([&] { const float4 r_ = kg_ld(n); return make_float2(r_.x, r_.y); }())
+#define IL_NKB(n) ([&] { const float4 r_ = kg_ld(n); return make_float2(r_.z, r_.w); }())
+#else
     float2 Kg[NT], nKb[NT];
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -291,6 +317,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         Kg[n] = make_float2((float)(Ks * gv_p[i]), (float)(Ks * gv_p[i + 1]));
         nKb[n] = make_float2((float)(-Ks * bv_p[i]), (float)(-Ks * bv_p[i + 1]));
     }
+    auto kg4 = [&](int n) { return make_float4(Kg[n].x, Kg[n].y, nKb[n].x, nKb[n].y); };
+#define IL_KG(n) Kg[n]
+#define IL_NKB(n) nKb[n]
+#endif
     __syncwarp();
 
 #if IL_LOOP2 || IL_FUSE1
@@ -315,7 +345,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
                     v[h][n] = __fadd2_rn(xA[h][n], xB[h][n]);
-                    p2 = __ffma2_rn(nKb[n], v[h][n], p2);
+                    p2 = __ffma2_rn(IL_NKB(n), v[h][n], p2);
                 }
                 pb[h] = p2.x + p2.y;
             }
@@ -325,8 +355,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
                     v[h][n] = __fadd2_rn(xA[h][n], xB[h][n]);
-                    pb[h] = fmaf(nKb[n].x, v[h][n].x, pb[h]);
-                    pb[h] = fmaf(nKb[n].y, v[h][n].y, pb[h]);
+                    pb[h] = fmaf(IL_NKB(n).x, v[h][n].x, pb[h]);
+                    pb[h] = fmaf(IL_NKB(n).y, v[h][n].y, pb[h]);
                 }
 #endif
             // aux states of both anneals of the quad, from their owner lanes
@@ -444,9 +474,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #else
                     const float2 m2 = make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
 #endif
-                    const float2 u2 = __ffma2_rn(nKb[n], make_float2(xah, xah), m2);
-                    CA[h][n] = __ffma2_rn(Kg[n], xA[h][n], u2);
-                    CB[h][n] = __ffma2_rn(Kg[n], xB[h][n], u2);
+                    const float4 kk = kg4(n);
+                    const float2 u2 = __ffma2_rn(make_float2(kk.z, kk.w), make_float2(xah, xah), m2);
+                    CA[h][n] = __ffma2_rn(make_float2(kk.x, kk.y), xA[h][n], u2);
+                    CB[h][n] = __ffma2_rn(make_float2(kk.x, kk.y), xB[h][n], u2);
 #if IL_FUSE_Q
                     xA[h][n] = __ffma2_rn(eA[h][n], CA[h][n], __fmul2_rn(xA[h][n], qA[h][n]));
                     xB[h][n] = __ffma2_rn(eB[h][n], CB[h][n], __fmul2_rn(xB[h][n], qB[h][n]));
@@ -609,8 +640,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             for (int n = 0; n < NT; ++n) {
                 q = fmaf(u[h][n].x, acc[n][2 * h], q);
                 q = fmaf(u[h][n].y, acc[n][2 * h + 1], q);
-                l = fmaf(nKb[n].x, u[h][n].x, l);
-                l = fmaf(nKb[n].y, u[h][n].y, l);
+                l = fmaf(IL_NKB(n).x, u[h][n].x, l);
+                l = fmaf(IL_NKB(n).y, u[h][n].y, l);
             }
             float e = fmaf(xa_h[h] >= 0.f ? 2.f : -2.f, l, q);  // -Ks (u'Gu + 2 s_aux b'u)
             e += __shfl_xor_sync(0xffffffffu, e, 1);
@@ -623,7 +654,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         double m = fmin(es[0], es[1]);
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) m = fmin(m, __shfl_xor_sync(0xffffffffu, m, o));
-        const double lim = m + 0x1p-11 * reinterpret_cast<const double*>(frag + L::kWarpF4 - 1)[0];
+        const double lim = m + 0x1p-11 * reinterpret_cast<const double*>(frag + L::kKgF4 - 1)[0];
         // lane 4g + h stands for row g + 8h (h < 2)
         const int hs = t & 1;
         const uint64_t my_pos = pos[hs], my_neg = neg[hs];
