@@ -298,6 +298,41 @@ def other_configs(dev, prm) -> dict:
     return res
 
 
+def stage_bytes(n_r: int, n_t: int, n_anneals: int) -> dict:
+    """Algorithmic HBM bytes per RE of the streaming stages (complex128 H, y
+    as the reference holds them; FP64 G, g, b out; int8 spins in)."""
+    N = 2 * n_t
+    S = 2 * N + 1
+    Bs = (n_anneals + 15) // 16 * 16
+    front = (16 * n_r * n_t + 16 * n_r + 8) + (8 * N * N + 16 * N + 8 * 4 + 2 * n_t + 1)
+    select = (Bs * S + Bs + 8 * Bs + 16 * n_r * n_t + 16 * n_r + 8 + 2 * n_t + 8) + (2 * n_t + 8 + 1 + 4 + 4)
+    return {"front": front, "select": select}
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def stage_rooflines(prof, steps, P, n_anneals) -> dict:
+    """HBM roofline of the streaming stages: algorithmic bytes
+    per step / kernel time against the measured copy bandwidth."""
+    peak, src = hbm_peak()
+    out = {}
+    for kind, nbytes in stage_bytes(N_R, N_T, n_anneals).items():
+        ms = prof.get(kind, (0.0, 0))[0] / max(steps, 1)
+        gbs = nbytes * P / (ms * 1e-3) / 1e9 if ms > 0 else None
+        bound = ("latency (FP64 elimination / Householder chains)" if kind == "front"
+                 else "HBM + latency (TMA-staged H, y; int8 spins)")
+        out[kind] = {"bound": bound, "bytes_per_re": nbytes,
+                     "achieved": gbs, "peak": peak, "unit": "GB/s",
+                     "frac": gbs / peak if gbs else None, "peak_source": src}
+    return out
+
+
 def workload_config(args) -> dict:
     return {"workload": "16x16 16-QAM uplink full slot (273 PRB x 12 sc x 14 sym = 45864 REs), "
                         "i.i.d. Rayleigh, 20 dB",
@@ -497,7 +532,8 @@ def run_ours(args) -> None:
                      "anneal_ms_per_launch": an_ms / max(an_n, 1),
                      "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
                      "traffic": anneal_traffic(),
-                     "traffic_unit": "bytes per launch (dram read + write, ncu --set full)"},
+                     "traffic_unit": "bytes per launch (dram read + write, ncu --set full)",
+                     "stages": stage_rooflines(prof, args.steps, P, prm.n_anneals)},
         "clocks": clk,
         "ser_check": ser,
         "other_configs": others,
