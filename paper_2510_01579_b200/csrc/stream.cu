@@ -139,9 +139,17 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
         cudaError_t e = cudaMallocAsync((void**)&b.dev, b.bytes * P, ss.in);
         if (e != cudaSuccess) rc = fail_cuda(e, "cudaMallocAsync(pipeline)");
     }
+    // ISINGLINK_PIPE_TRACE=2: per-chunk device timeline (timing events)
+    std::vector<cudaEvent_t> tev;
+    const bool timeline = env_int("ISINGLINK_PIPE_TRACE", 0) > 1;
+    if (timeline) {
+        tev.resize(3 * K + 1);
+        for (cudaEvent_t& e : tev) cudaEventCreate(&e);
+    }
     if (rc == IL_OK) {
         cudaEvent_t ready = ss.ev[2 * K];
         cudaEventRecord(ready, ss.in);
+        if (timeline) cudaEventRecord(tev[3 * K], ss.in);
         for (int k = 0; k < n_comp; ++k) cudaStreamWaitEvent(ss.comp[k], ready, 0);
         cudaStreamWaitEvent(ss.out, ready, 0);
         for (int c = 0; c < K && rc == IL_OK; ++c) {
@@ -151,11 +159,14 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
                     cudaMemcpyAsync(b.dev + o * b.bytes, (const char*)b.host_in + o * b.bytes,
                                     n * b.bytes, cudaMemcpyHostToDevice, ss.in);
             cudaEventRecord(ss.ev[2 * c], ss.in);
+            if (timeline) cudaEventRecord(tev[3 * c], ss.in);
             cudaStream_t cs = ss.comp[c % n_comp];
             cudaStreamWaitEvent(cs, ss.ev[2 * c], 0);
+            if (timeline) cudaEventRecord(tev[3 * c + 1], cs);
             rc = compute(o, n, cs);
             if (rc) break;
             cudaEventRecord(ss.ev[2 * c + 1], cs);
+            if (timeline) cudaEventRecord(tev[3 * c + 2], cs);
         }
         for (int c = 0; c < K && rc == IL_OK; ++c) {
             const int64_t o = bounds[c], n = bounds[c + 1] - o;
@@ -180,6 +191,18 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
         auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
         fprintf(stderr, "[pipe] P=%lld chunks=%d enqueue %.1f us, total %.1f us\n", (long long)P, K,
                 us(t_start, t_enq), us(t_start, t_end));
+    }
+    if (timeline) {
+        cudaDeviceSynchronize();
+        for (int c = 0; c < K; ++c) {
+            float h = 0, a = 0, b = 0;
+            cudaEventElapsedTime(&h, tev[3 * K], tev[3 * c]);
+            cudaEventElapsedTime(&a, tev[3 * K], tev[3 * c + 1]);
+            cudaEventElapsedTime(&b, tev[3 * K], tev[3 * c + 2]);
+            fprintf(stderr, "[pipe] chunk %2d n=%6lld h2d_done %.3f  compute %.3f -> %.3f ms\n", c,
+                    (long long)(bounds[c + 1] - bounds[c]), h, a, b);
+        }
+        for (cudaEvent_t& ev : tev) cudaEventDestroy(ev);
     }
     if (rc == IL_OK && e != cudaSuccess) rc = fail_cuda(e, "host pipeline");
     return rc;
