@@ -92,6 +92,7 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
     static const int cap_div = env_int("ISINGLINK_PIPE_CAP_DIV", IL_PIPE_CAP_DIV);
     static const int first_div = env_int("ISINGLINK_PIPE_FIRST_DIV", IL_PIPE_FIRST_DIV);
     static const bool taper = env_int("ISINGLINK_PIPE_TAPER", IL_PIPE_TAPER + 1) > 1;
+    static const int align = env_int("ISINGLINK_PIPE_ALIGN", 0);
     std::vector<int64_t> bounds{0};
     if (n_chunks > 0 || P < 4096) {
         if (n_chunks <= 0) n_chunks = 1;
@@ -100,10 +101,14 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
         chunk = (chunk + 7) / 8 * 8;
         while (bounds.back() < P) bounds.push_back(std::min(P, bounds.back() + chunk));
     } else {
-        const int64_t cap = std::max<int64_t>(P / cap_div, 8);
+        int64_t cap = std::max<int64_t>(P / cap_div, 8);
         int64_t c = std::max<int64_t>(P / first_div, 256);
+        if (align > 0) {  // whole anneal waves: first chunk one wave, cap a multiple
+            c = align;
+            cap = std::max<int64_t>(cap / align, 1) * align;
+        }
         while (bounds.back() < P) {
-            int64_t cc = (std::min(c, cap) + 7) / 8 * 8;
+            int64_t cc = align > 0 ? std::min(c, cap) : (std::min(c, cap) + 7) / 8 * 8;
             // taper: the last chunks halve (its anneal tail has no next
             // chunk to overlap with)
             const int64_t rem = P - bounds.back();
