@@ -220,6 +220,19 @@ int il_detect_cim_host(const double* H, const double* y, const double* noise_var
                        double* energy, int8_t* source, int32_t* anneal_index,
                        int32_t* diverged_count, int32_t n_chunks);
 
+/* Streaming form of il_detect_cim_host: enqueues the same pipeline and
+ * returns at once with *ticket; il_pipeline_wait(ticket) returns when the
+ * outputs are in host memory (inputs must stay valid until then).  Slots
+ * submitted back to back share the device streams, so the copies and the
+ * first chunks of slot s+1 overlap the tail of slot s.  *ticket is NULL
+ * (nothing to wait for) when P == 0. */
+int il_detect_cim_host_submit(const double* H, const double* y, const double* noise_var,
+                              int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                              const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
+                              double* energy, int8_t* source, int32_t* anneal_index,
+                              int32_t* diverged_count, int32_t n_chunks, void** ticket);
+int il_pipeline_wait(void* ticket);
+
 /* Host-buffer form of il_precode_vpp_batch (every pointer HOST memory),
  * streamed through the device in n_chunks pieces (<= 0: auto) like
  * il_detect_cim_host. */

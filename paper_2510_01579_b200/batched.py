@@ -13,6 +13,7 @@ reference-shaped per-instance API in ``api.py`` is built on them.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -103,14 +104,36 @@ def _host(x, dtype: torch.dtype, shape) -> torch.Tensor:
     return t
 
 
-def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
-                    precision: str | None = None, n_chunks: int = 0, out=None) -> DetectBatch:
-    """P x ``detect_cim`` from HOST buffers to HOST buffers.
+class HostTicket:
+    """A slot submitted with ``detect_cim_host_submit``: ``wait()`` returns
+    its DetectBatch once the outputs are in host memory.  Holds the input
+    and output buffers alive until then."""
 
-    The slot is streamed through the GPU in chunks with H2D copy, detection
-    and D2H copy overlapped (il_detect_cim_host).  Pass pinned CPU tensors
-    (``tensor.pin_memory()``) for the overlap; ``out`` may hold preallocated
-    (pinned) output tensors in DetectBatch layout."""
+    def __init__(self, handle, out, keep):
+        self._handle, self.out, self._keep = handle, out, keep
+
+    def wait(self) -> DetectBatch:
+        if self._keep is not None:
+            h, self._handle = self._handle, None
+            self._keep_alive, self._keep = self._keep, None
+            _lib.call("il_pipeline_wait", h)
+            self._keep_alive = None
+        return self.out
+
+    def __del__(self):  # never release buffers a copy may still be using
+        try:
+            self.wait()
+        except Exception:
+            pass
+
+
+def detect_cim_host_submit(H, y, noise_var, order: int, seeds, params=None,
+                           precision: str | None = None, n_chunks: int = 0,
+                           out=None) -> HostTicket:
+    """Streaming form of ``detect_cim_host`` (il_detect_cim_host_submit):
+    enqueue the slot and return a ticket at once.  Slots submitted back to
+    back overlap: the next slot's copies and first chunks run under this
+    slot's tail."""
     params = params or CacParams()
     prm = to_c(params, precision)
     Ht = H if isinstance(H, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(H))
@@ -132,11 +155,24 @@ def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
                           source=torch.empty(P, dtype=torch.int8, pin_memory=pin),
                           anneal_index=torch.empty(P, dtype=torch.int32, pin_memory=pin),
                           diverged=torch.empty(P, dtype=torch.int32, pin_memory=pin))
-    _lib.call("il_detect_cim_host", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(), P, n_r, n_t,
-              int(order), st.data_ptr(), prm, out.x_idx.data_ptr(), out.energy.data_ptr(),
+    handle = ctypes.c_void_p()
+    _lib.call("il_detect_cim_host_submit", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(), P, n_r,
+              n_t, int(order), st.data_ptr(), prm, out.x_idx.data_ptr(), out.energy.data_ptr(),
               out.source.data_ptr(), out.anneal_index.data_ptr(), out.diverged.data_ptr(),
-              int(n_chunks))
-    return out
+              int(n_chunks), ctypes.byref(handle))
+    return HostTicket(handle, out, (Hh, yh, sh, st))
+
+
+def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
+                    precision: str | None = None, n_chunks: int = 0, out=None) -> DetectBatch:
+    """P x ``detect_cim`` from HOST buffers to HOST buffers.
+
+    The slot is streamed through the GPU in chunks with H2D copy, detection
+    and D2H copy overlapped (il_detect_cim_host).  Pass pinned CPU tensors
+    (``tensor.pin_memory()``) for the overlap; ``out`` may hold preallocated
+    (pinned) output tensors in DetectBatch layout."""
+    return detect_cim_host_submit(H, y, noise_var, order, seeds, params, precision, n_chunks,
+                                  out).wait()
 
 
 @dataclass

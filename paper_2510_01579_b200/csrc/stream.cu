@@ -21,7 +21,7 @@
 using namespace il;
 
 #ifndef IL_PIPE_CAP_DIV
-#define IL_PIPE_CAP_DIV 16
+#define IL_PIPE_CAP_DIV 8
 #endif
 #ifndef IL_PIPE_TAPER  // halve the last chunks (env ISINGLINK_PIPE_TAPER=2 on, 1 off)
 #define IL_PIPE_TAPER 0
@@ -87,7 +87,8 @@ int env_int(const char* name, int dflt) {
 
 // Chunk boundaries: n_chunks > 0 -> equal chunks; otherwise (P >= 4096) a
 // ramp: a small first chunk (~P/48, its H2D is the exposed latency) doubling
-// up to P/16, so few chunks carry wave tails.
+// up to P/8, so few chunks carry wave tails (streamed slots: 5.54 ms/slot at
+// P/8 vs 5.6-5.7 at P/16; one slot at a time the cap is flat).
 std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
     static const int cap_div = env_int("ISINGLINK_PIPE_CAP_DIV", IL_PIPE_CAP_DIV);
     static const int first_div = env_int("ISINGLINK_PIPE_FIRST_DIV", IL_PIPE_FIRST_DIV);
@@ -124,8 +125,12 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
 // on alternating compute streams once its inputs landed, D2H of the outputs
 // on `out` (enqueued last: a copy into pageable memory blocks the host
 // thread and must not delay the enqueue of later chunks).
+// done == nullptr: synchronous (returns when the outputs are in host memory);
+// otherwise *done receives an event recorded after the last D2H copy and the
+// call returns once everything is enqueued (il_pipeline_wait completes it).
 template <class F>
-int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& compute) {
+int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& compute,
+                 cudaEvent_t* done = nullptr) {
     keep_pool_warm();
     static const bool trace = env_int("ISINGLINK_PIPE_TRACE", 0) > 0;
     const auto t_start = std::chrono::steady_clock::now();
@@ -190,6 +195,12 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
     for (PipeBuf& b : bufs)
         if (b.dev) cudaFreeAsync(b.dev, ss.out);
     const auto t_enq = std::chrono::steady_clock::now();
+    if (done && rc == IL_OK) {
+        cudaError_t e = cudaEventCreateWithFlags(done, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(*done, ss.out);
+        if (e == cudaSuccess) return IL_OK;
+        rc = fail_cuda(e, "host pipeline (submit)");
+    }
     cudaError_t e = cudaStreamSynchronize(ss.out);
     if (trace) {
         const auto t_end = std::chrono::steady_clock::now();
@@ -215,11 +226,52 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
 
 }  // namespace
 
+namespace {
+int detect_host(const double* H, const double* y, const double* noise_var, int64_t P, int32_t n_r,
+                int32_t n_t, int32_t qam_order, const uint64_t* seed, const il_cac_params* prm,
+                uint8_t* x_idx, double* energy, int8_t* source, int32_t* anneal_index,
+                int32_t* diverged_count, int32_t n_chunks, cudaEvent_t* done);
+}
+
 extern "C" int il_detect_cim_host(const double* H, const double* y, const double* noise_var,
                                   int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
                                   const uint64_t* seed, const il_cac_params* prm, uint8_t* x_idx,
                                   double* energy, int8_t* source, int32_t* anneal_index,
                                   int32_t* diverged_count, int32_t n_chunks) {
+    return detect_host(H, y, noise_var, P, n_r, n_t, qam_order, seed, prm, x_idx, energy, source,
+                       anneal_index, diverged_count, n_chunks, nullptr);
+}
+
+extern "C" int il_detect_cim_host_submit(const double* H, const double* y,
+                                         const double* noise_var, int64_t P, int32_t n_r,
+                                         int32_t n_t, int32_t qam_order, const uint64_t* seed,
+                                         const il_cac_params* prm, uint8_t* x_idx, double* energy,
+                                         int8_t* source, int32_t* anneal_index,
+                                         int32_t* diverged_count, int32_t n_chunks,
+                                         void** ticket) {
+    IL_REQUIRE(ticket, "ticket must not be NULL");
+    *ticket = nullptr;
+    cudaEvent_t done = nullptr;
+    const int rc = detect_host(H, y, noise_var, P, n_r, n_t, qam_order, seed, prm, x_idx, energy,
+                               source, anneal_index, diverged_count, n_chunks, &done);
+    if (rc == IL_OK) *ticket = done;  // nullptr when P == 0: nothing to wait for
+    return rc;
+}
+
+extern "C" int il_pipeline_wait(void* ticket) {
+    if (!ticket) return IL_OK;
+    cudaEvent_t ev = static_cast<cudaEvent_t>(ticket);
+    const cudaError_t e = cudaEventSynchronize(ev);
+    cudaEventDestroy(ev);
+    if (e != cudaSuccess) return fail_cuda(e, "host pipeline (wait)");
+    return IL_OK;
+}
+
+namespace {
+int detect_host(const double* H, const double* y, const double* noise_var, int64_t P, int32_t n_r,
+                int32_t n_t, int32_t qam_order, const uint64_t* seed, const il_cac_params* prm,
+                uint8_t* x_idx, double* energy, int8_t* source, int32_t* anneal_index,
+                int32_t* diverged_count, int32_t n_chunks, cudaEvent_t* done) {
     IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
                "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
     IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && x_idx), "NULL buffer");
@@ -236,8 +288,9 @@ extern "C" int il_detect_cim_host(const double* H, const double* y, const double
                                    (const double*)at(2), n, n_r, n_t, qam_order,
                                    (const uint64_t*)at(3), prm, (uint8_t*)at(4), (double*)at(5),
                                    (int8_t*)at(6), (int32_t*)at(7), (int32_t*)at(8), cs);
-    });
+    }, done);
 }
+}  // namespace
 
 extern "C" int il_precode_vpp_host(const double* H, const double* u, int64_t P, int32_t n_u,
                                    int32_t n_ant, double power, double tau, int32_t n_stages,

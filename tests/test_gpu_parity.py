@@ -218,6 +218,33 @@ def test_detect_cim_host_pipeline_matches_device_batch(n_chunks):
             assert np.array_equal(host.x_idx.numpy()[:n], d["x_hat"])
 
 
+def test_detect_cim_host_submit_streams_slots():
+    """Back-to-back submitted slots (il_detect_cim_host_submit) overlap on the
+    device streams but each returns exactly the synchronous result; an empty
+    slot yields a NULL ticket."""
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    d = load_golden("d16x16_16qam_20db.npz")
+    reps = 40
+    H = torch.from_numpy(np.concatenate([d["H"]] * reps)).pin_memory()
+    y = torch.from_numpy(np.concatenate([d["y"]] * reps)).pin_memory()
+    s2 = torch.from_numpy(np.concatenate([d["noise_var"]] * reps)).pin_memory()
+    seed = np.concatenate([d["seed"]] * reps)
+    prm = CacParams(precision="fp32")
+    want = batched.detect_cim_host(H, y, s2, int(d["order"]), seed, prm)
+    tickets = [batched.detect_cim_host_submit(H, y, s2, int(d["order"]), seed, prm)
+               for _ in range(3)]
+    for tk in tickets:
+        got = tk.wait()
+        for f in ("x_idx", "energy", "source", "anneal_index", "diverged"):
+            assert torch.equal(getattr(want, f), getattr(got, f)), f
+    empty = batched.detect_cim_host_submit(torch.zeros((0, 4, 4), dtype=torch.complex128),
+                                           torch.zeros((0, 4), dtype=torch.complex128),
+                                           torch.zeros(0, dtype=torch.float64), 16,
+                                           np.zeros(0, np.uint64))
+    assert empty.wait().x_idx.shape == (0, 4, 2)
+
+
 def test_detect_cim_host_rejects_device_buffers():
     from paper_2510_01579_b200 import batched
     H = torch.zeros((2, 4, 4), dtype=torch.complex128, device="cuda")
