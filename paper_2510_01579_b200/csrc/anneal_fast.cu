@@ -54,12 +54,6 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_FAST_MINB
 #define IL_FAST_MINB 3
 #endif
-#ifndef IL_LOOP2  // refresh-period outer loop, f_mvm Euler steps inner
-#define IL_LOOP2 0
-#endif
-#ifndef IL_FUSE1  // as IL_LOOP2, first Euler step fused into the refresh block
-#define IL_FUSE1 0
-#endif
 #ifndef IL_NOUTER  // MMA issue order: n-tile outer (early accumulators)
 #define IL_NOUTER 0
 #endif
@@ -86,12 +80,6 @@ constexpr int kWarpsPerCta = 4;
 #endif
 #ifndef IL_PROBE_NO_RNG  // timing probe only: constant initial states (wrong output)
 #define IL_PROBE_NO_RNG 0
-#endif
-#if IL_FUSE_Q && (IL_FUSE1 || IL_LOOP2)
-#error "IL_FUSE_Q is implemented for the default loop structure only"
-#endif
-#if IL_BOUND_FLOOR && (IL_FUSE1 || IL_LOOP2)
-#error "IL_BOUND_FLOOR is implemented for the default loop structure only"
 #endif
 
 template <int NT>
@@ -326,15 +314,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #endif
     __syncwarp();
 
-#if IL_LOOP2 || IL_FUSE1
-    for (int step0 = 0; step0 < s.n_steps; step0 += s.f_mvm) {
-        {
-#else
     int until_refresh = 0;
     for (int step = 0; step < s.n_steps; ++step) {
         if (until_refresh == 0) {
             until_refresh = s.f_mvm;
-#endif
             // ---- refresh: v = x1 + x2, M' = -Ks G v on tensor cores -----------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
@@ -503,24 +486,6 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         else
 #endif
         {
-#if IL_FUSE1
-        // first Euler step of the period in the refresh's basic block
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-                euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, e_floor, dv[h][n & 1]);
-                euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
-            }
-        }
-        euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
-        const int n_in = min(s.f_mvm, s.n_steps - step0);
-        for (int k = 1; k < n_in; ++k) {
-#elif IL_LOOP2
-        const int n_in = min(s.f_mvm, s.n_steps - step0);
-#pragma unroll 2
-        for (int k = 0; k < n_in; ++k) {
-#endif
 #if IL_EULER_GROUP
         // the same per-pair operations as euler_pair, issued stage by stage
         // over groups of 4 spin pairs so that dependent instructions are 4
@@ -595,11 +560,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         }
 #endif
         euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
-#if IL_LOOP2 || IL_FUSE1
-        }
-#else
         --until_refresh;
-#endif
     }
 
     // ---- epilogue: divergence flags, spins, FP64 energies --------------------
