@@ -54,6 +54,9 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_FAST_MINB
 #define IL_FAST_MINB 3
 #endif
+#ifndef IL_FAST_MINB2  // CTAs per SM for N <= 16
+#define IL_FAST_MINB2 4
+#endif
 #ifndef IL_NOUTER  // MMA issue order: n-tile outer (early accumulators)
 #define IL_NOUTER 0
 #endif
@@ -113,7 +116,7 @@ struct FastLayout {
 // leaves e*C unchanged, and e' = max(floor, e r) becomes
 // e_s' = max(floor * 2^-sc, e_s r) -- power-of-two scalings are exact.
 template <int NT, bool SPLIT, bool SAME_QR>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, NT <= 2 ? 4 : (NT <= 4 ? IL_FAST_MINB : 1))
+__global__ void __launch_bounds__(kWarpsPerCta * 32, NT <= 2 ? IL_FAST_MINB2 : (NT <= 4 ? IL_FAST_MINB : 1))
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
               const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
@@ -649,7 +652,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             e += __shfl_xor_sync(0xffffffffu, e, 1);
             e += __shfl_xor_sync(0xffffffffu, e, 2);
             // padded rows (>= b_valid) never enter the selection
-            es[h] = (dflag[h] || mt * 16 + g + 8 * h >= s.b_valid) ? INFINITY : (double)e * (-1.0 / Ks);
+            // (a zero coupling scale leaves no screen: every survivor is a candidate)
+            es[h] = (dflag[h] || mt * 16 + g + 8 * h >= s.b_valid) ? INFINITY
+                    : (Ks > 0.0 ? (double)e * (-1.0 / Ks) : 0.0);
         }
         // tile minimum over survivors; candidates within 2 x 2^-12 mag of it
         // (the screen error is < 2^-13 mag, see launch_anneal_fast)

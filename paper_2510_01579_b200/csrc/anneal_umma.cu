@@ -481,7 +481,9 @@ k_anneal_umma(const double* __restrict__ Gall, const double* __restrict__ gall,
             float e = fmaf(xa_h[h] >= 0.f ? 2.f : -2.f, l, q);
             e += __shfl_xor_sync(0xffffffffu, e, 1);
             e += __shfl_xor_sync(0xffffffffu, e, 2);
-            es[h] = (dflag[h] || mt * 16 + g + 8 * h >= s.b_valid) ? INFINITY : (double)e * (-1.0 / Ks);
+            // (a zero coupling scale leaves no screen: every survivor is a candidate)
+            es[h] = (dflag[h] || mt * 16 + g + 8 * h >= s.b_valid) ? INFINITY
+                    : (Ks > 0.0 ? (double)e * (-1.0 / Ks) : 0.0);
         }
     }
     // TMEM is no longer needed by any warp
