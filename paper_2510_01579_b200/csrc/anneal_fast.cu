@@ -126,6 +126,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     constexpr int N = L::N;
     constexpr int S = L::S;
     constexpr int KT = L::KT;
+    // scaled state (IL_SCALED_X): x~ = sqrt(dt) x wherever x is stored
+    constexpr bool SC = IL_SCALED_X && SAME_QR;
+    static_assert(!(SC && (IL_FUSE_Q || IL_EULER_GROUP)), "variants assume the unscaled state");
     extern __shared__ __align__(16) uint4 smem_u4[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerCta + warp;
@@ -202,14 +205,16 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             const int ia = i0 + i, ib = i0 + Lseg + i;
             const double ua = rng.uniform(s.x0_lo, s.x0_range);
             const double ub = r2.uniform(s.x0_lo, s.x0_range);
-            if (ia < S) row[ia] = (float)ua;
-            if (ib < S) row[ib] = (float)ub;
+            if (ia < S) row[ia] = SC ? (float)(s.sdt * ua) : (float)ua;
+            if (ib < S) row[ib] = SC ? (float)(s.sdt * ub) : (float)ub;
         }
         } else {
         constexpr int S0 = (S + 1) / 2;
         if (part) rng.state = add128(mul128(rng.state, s.jump_mult[3]), mul128(rng.inc, s.jump_add[3]));
         const int i0 = part ? S0 : 0, i1 = part ? S : S0;
-        for (int i = i0; i < i1; ++i) x0s[al * S + i] = (float)rng.uniform(s.x0_lo, s.x0_range);
+        for (int i = i0; i < i1; ++i)
+            x0s[al * S + i] = SC ? (float)(s.sdt * rng.uniform(s.x0_lo, s.x0_range))
+                                 : (float)rng.uniform(s.x0_lo, s.x0_range);
         }
     }
     }
@@ -256,8 +261,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             CA[h][n] = CB[h][n] = make_float2(0.f, 0.f);
         }
     }
-    float xa = x0s[(g + 8 * hown) * S + 2 * N], ea = e_init, Ca = 0.f, dva = 0.f;
-    float dv[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+    // divergence tracking: sticky max of x^2, or (SC) sticky min of q
+    constexpr float kD0 = SC ? INFINITY : 0.f;
+    float xa = x0s[(g + 8 * hown) * S + 2 * N], ea = e_init, Ca = 0.f, dva = kD0;
+    float dv[2][2] = {{kD0, kD0}, {kD0, kD0}};
 #if IL_BOUND_FLOOR
     float e_lb = e_init;  // lower bound of every eA/eB of this thread
 #endif
@@ -530,8 +537,13 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int n = 0; n < NT; ++n) {
-                euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, e_floor, dv[h][n & 1]);
-                euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
+                if constexpr (SC) {
+                    euler_pair_sc(xA[h][n], eA[h][n], CA[h][n], s.alpha, dv[h][n & 1]);
+                    euler_pair_sc(xB[h][n], eB[h][n], CB[h][n], s.alpha, dv[h][n & 1]);
+                } else {
+                    euler_pair<SAME_QR>(xA[h][n], eA[h][n], CA[h][n], s, e_floor, dv[h][n & 1]);
+                    euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
+                }
             }
         }
 #endif
@@ -545,8 +557,14 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         // floor can bind and the 2 FMNMX per spin pair are skipped; otherwise
         // every element is clamped exactly as before (also for NaN).
         {
-            const float dmax = max_nan3(max_nan(dv[0][0], dv[0][1]), dv[1][0], dv[1][1]);
-            const float r_lb = SAME_QR ? fmaf(s.ndt, dmax, s.alpha) : fmaf(s.ndtz, dmax, s.beta);
+            // (SC: the sticky minimum of q is itself the smallest factor)
+            const float r_lb = SC ? min_nan3(min_nan(dv[0][0], dv[0][1]), dv[1][0], dv[1][1])
+                                  : [&] {
+                                        const float dmax = max_nan3(max_nan(dv[0][0], dv[0][1]),
+                                                                    dv[1][0], dv[1][1]);
+                                        return SAME_QR ? fmaf(s.ndt, dmax, s.alpha)
+                                                       : fmaf(s.ndtz, dmax, s.beta);
+                                    }();
             const float nxt = e_lb * r_lb;
             if (nxt >= e_floor) {
                 e_lb = nxt;
@@ -562,7 +580,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             }
         }
 #endif
-        euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
+        if constexpr (SC)
+            euler_one_sc(xa, ea, Ca, s.alpha, e_floor, dva);
+        else
+            euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
         --until_refresh;
     }
 
@@ -570,8 +591,25 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     // E = u'Gu - 2 tr G + 2 s_aux b'u with u = s_A + s_B (solver.py:171-175)
     const float xa_h[2] = {__shfl_sync(0xffffffffu, xa, (lane & ~3) | 0),
                            __shfl_sync(0xffffffffu, xa, (lane & ~3) | 1)};
-    float dvh[2] = {max_nan(dv[0][0], dv[0][1]), max_nan(dv[1][0], dv[1][1])};
-    dvh[hown] = max_nan(dvh[hown], max_nan(dva, xa * xa));  // own aux spin
+    // the final state enters the divergence test too
+    auto dfold = [&](float d, float a, float b) {
+        if constexpr (SC)
+            return min_nan3(d, fmaf(-a, a, s.alpha), fmaf(-b, b, s.alpha));
+        else
+            return max_nan3(d, a * a, b * b);
+    };
+    auto dmerge = [&](float a, float b) {
+        if constexpr (SC)
+            return min_nan(a, b);
+        else
+            return max_nan(a, b);
+    };
+    float dvh[2] = {dmerge(dv[0][0], dv[0][1]), dmerge(dv[1][0], dv[1][1])};
+    // own aux spin: its tracked value and its final state
+    if constexpr (SC)
+        dvh[hown] = min_nan(dvh[hown], min_nan(dva, fmaf(-xa, xa, s.alpha)));
+    else
+        dvh[hown] = max_nan(dvh[hown], max_nan(dva, xa * xa));
     const int64_t row0 = prob * (int64_t)B + mt * 16;
     uint64_t pos[2], neg[2];
     bool dflag[2];
@@ -583,8 +621,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         int8_t* sp = spins + row * S;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-            d = max_nan3(d, xA[h][n].x * xA[h][n].x, xA[h][n].y * xA[h][n].y);
-            d = max_nan3(d, xB[h][n].x * xB[h][n].x, xB[h][n].y * xB[h][n].y);
+            d = dfold(d, xA[h][n].x, xA[h][n].y);
+            d = dfold(d, xB[h][n].x, xB[h][n].y);
             const int i = 8 * n + 2 * t;
             const int a0 = xA[h][n].x >= 0.f ? 1 : -1, a1 = xA[h][n].y >= 0.f ? 1 : -1;
             const int b0 = xB[h][n].x >= 0.f ? 1 : -1, b1 = xB[h][n].y >= 0.f ? 1 : -1;
@@ -595,8 +633,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             pm |= (uint64_t)(a0 + b0 == 2) << i | (uint64_t)(a1 + b1 == 2) << (i + 1);
             nm |= (uint64_t)(a0 + b0 == -2) << i | (uint64_t)(a1 + b1 == -2) << (i + 1);
         }
-        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 1));
-        d = max_nan(d, __shfl_xor_sync(0xffffffffu, d, 2));
+        d = dmerge(d, __shfl_xor_sync(0xffffffffu, d, 1));
+        d = dmerge(d, __shfl_xor_sync(0xffffffffu, d, 2));
         pm |= __shfl_xor_sync(0xffffffffu, pm, 1);
         pm |= __shfl_xor_sync(0xffffffffu, pm, 2);
         nm |= __shfl_xor_sync(0xffffffffu, nm, 1);
@@ -604,7 +642,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         pos[h] = pm;
         neg[h] = nm;
         if (t == h) sp[2 * N] = xa >= 0.f ? 1 : -1;
-        dflag[h] = !(d <= s.thr2);
+        dflag[h] = SC ? !(d >= s.qthr) : !(d <= s.thr2);
         if (t == 0) diverged[row] = dflag[h] ? 1 : 0;
     }
     if (screened) {
@@ -855,6 +893,8 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.x0_range = s.x0_range;
     fs.f_mvm = s.f_mvm;
     fs.n_steps = s.n_steps;
+    fs.sdt = sqrt(s.dt);
+    fs.qthr = (float)(1.0 + s.dt * (s.p - 1.0) - s.dt * s.thr * s.thr);
     fs.b_valid = screen_rows;
     // the screen pays off from N = 24 on (at N = 16 the FP64 epilogue is cheaper)
     // ISINGLINK_SCREEN=0 turns the screen off (the parity test compares both)

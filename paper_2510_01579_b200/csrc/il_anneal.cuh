@@ -16,6 +16,10 @@
 namespace il {
 namespace fastk {
 
+#ifndef IL_SCALED_X  // state stored as sqrt(dt) x: the Euler factor is one FMA
+#define IL_SCALED_X 1
+#endif
+
 struct FastScalars {
     float alpha;    // 1 + dt (p - 1)
     float ndt;      // -dt
@@ -28,6 +32,8 @@ struct FastScalars {
     U128 jump_mult[4], jump_add[4];  // PCG64 advance by 1, 2, 3 quarter segments; [3]: half
     int f_mvm, n_steps;
     int n_slots;  // problems whose G a CTA stages (IL_TMA_G)
+    double sdt;   // sqrt(dt): scale of the stored state (IL_SCALED_X)
+    float qthr;   // alpha - dt thr^2: q below it means |x| > thr (IL_SCALED_X)
     int b_valid;  // anneal rows per problem that enter the selection (screened energies)
 };
 
@@ -114,6 +120,39 @@ __device__ __forceinline__ void euler_one(float& x, float& e, const float C, con
     const float r = SAME_QR ? q : fmaf(s.ndtz, x2, s.beta);
     x = fmaf(e, C, x * q);
     e = fmaxf(e * r, e_floor);
+}
+
+__device__ __forceinline__ float min_nan3(float a, float b, float c) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    asm("min.NaN.f32 %0, %0, %1;" : "+f"(r) : "f"(c));
+    return r;
+}
+__device__ __forceinline__ float min_nan(float a, float b) {
+    float r;
+    asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+    return r;
+}
+
+// Scaled-state Euler step (IL_SCALED_X, x- and e-factors equal): with
+// x~ = sqrt(dt) x the factor q = 1 + dt (p - 1) - dt x^2 = alpha - x~^2 is a
+// single FMA (x^2 is never formed), and |x| > thr <=> q < alpha - dt thr^2,
+// so the divergence test tracks the sticky NaN-propagating minimum of q.
+// The coupling term scales with the state (C~ = sqrt(dt) C is what the
+// refresh produces from x~), so x~' = x~ q + e C~.
+__device__ __forceinline__ void euler_pair_sc(float2& x, float2& e, const float2 C, float alpha,
+                                              float& qmin) {
+    const float2 q = __ffma2_rn(make_float2(-x.x, -x.y), x, make_float2(alpha, alpha));
+    qmin = min_nan3(qmin, q.x, q.y);
+    x = __ffma2_rn(e, C, __fmul2_rn(x, q));
+    e = __fmul2_rn(e, q);
+}
+__device__ __forceinline__ void euler_one_sc(float& x, float& e, const float C, float alpha,
+                                             float e_floor, float& qmin) {
+    const float q = fmaf(-x, x, alpha);
+    qmin = min_nan(qmin, q);
+    x = fmaf(e, C, x * q);
+    e = fmaxf(e * q, e_floor);
 }
 
 // PCG64 advance-by-k constants: state_k = M^k state_0 + inc * (M^{k-1} + ... + 1)
