@@ -908,7 +908,12 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     const bool split = precision != IL_PREC_TF32;
     // x and e share their per-step factor exactly when zeta*dt == dt and
     // 1 + dt (p - 1) == 1 + dt zeta a in FP32 (the reference defaults)
-    const bool same_qr = fs.alpha == fs.beta && fs.ndt == fs.ndtz;
+    // The scaled state (SAME_QR instantiations, IL_SCALED_X) tests divergence
+    // on q = alpha - dt x^2 against alpha - dt thr^2: keep the test's
+    // resolution (one ulp of q) below 2^-18 of dt thr^2, otherwise (tiny
+    // thresholds) take the general instantiation, which compares x^2 directly.
+    const bool same_qr = fs.alpha == fs.beta && fs.ndt == fs.ndtz &&
+                         (!IL_SCALED_X || s.dt * s.thr * s.thr >= fabs((double)fs.alpha) * 0x1p-6);
     if (use_umma() && umma_anneal_supported(N, B))
         return launch_anneal_umma(G, g, b, base_seed, eps_p, P, N, B, &fs, split, same_qr, spins,
                                   diverged, energies, screened, st);
