@@ -72,6 +72,9 @@ constexpr int kWarpsPerCta = 4;
 #ifndef IL_KG_SMEM  // refresh constants Kg, -Kb in shared memory (frees 4 NT registers)
 #define IL_KG_SMEM 1
 #endif
+#ifndef IL_CPLX_MVM  // 3-product (Karatsuba) coupling refresh for complex-structured G
+#define IL_CPLX_MVM 0  // measured 1.7% slower (the extra FP32 work outweighs 6 HMMA)
+#endif
 #ifndef IL_EULER_GROUP  // Euler step issued stage by stage over groups of 4 spin pairs
 #define IL_EULER_GROUP 0  // measured within noise (16x16 -0.3%, 8x8 +0.9%)
 #endif
@@ -115,7 +118,7 @@ struct FastLayout {
 // enters the update as e*C, so storing e_s = e * 2^-sc and C_s = C * 2^sc
 // leaves e*C unchanged, and e' = max(floor, e r) becomes
 // e_s' = max(floor * 2^-sc, e_s r) -- power-of-two scalings are exact.
-template <int NT, bool SPLIT, bool SAME_QR>
+template <int NT, bool SPLIT, bool SAME_QR, bool CPLX>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, NT <= 2 ? IL_FAST_MINB2 : (NT <= 4 ? IL_FAST_MINB : 1))
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
@@ -289,6 +292,32 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             frag[(kt * NT + n) * 32 + lane] = make_uint4(h01, h23, l01, l23);
         }
     }
+    if constexpr (CPLX) {
+        // G = [[R, -I], [I, R]] (n = N/2 = 16 KT/2 real spins first): the
+        // Karatsuba refresh needs B = -Ks (R - I) beside -Ks R (k-tiles of the
+        // real rows) and -Ks I (k-tiles of the imaginary rows), in the slots of
+        // the (real rows x imaginary columns) tiles it does not read
+        constexpr int KH = KT / 2, NH = NT / 2;
+#pragma unroll
+        for (int kt = 0; kt < KH; ++kt) {
+#pragma unroll
+            for (int n = 0; n < NH; ++n) {
+                const int c = 8 * n + g;
+                float f[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int r = 16 * kt + 2 * t + (q & 1) + 8 * (q >> 1);
+                    const double gr = L::kSmemG ? G[r * N + c] : __ldg(G + r * N + c);
+                    const double gi = L::kSmemG ? G[(r + N / 2) * N + c] : __ldg(G + (r + N / 2) * N + c);
+                    f[q] = (float)(-Ks * (gr - gi));
+                }
+                uint32_t h01, l01, h23, l23;
+                split_h2(make_float2(f[0], f[1]), h01, l01);
+                split_h2(make_float2(f[2], f[3]), h23, l23);
+                frag[(kt * NT + n + NH) * 32 + lane] = make_uint4(h01, h23, l01, l23);
+            }
+        }
+    }
     // per-thread spin constants: Ks g_i and -Ks b_i for spins 8n+2t+{0,1}
 #if IL_KG_SMEM
     // kept in shared memory and re-read at every refresh: the registers go to
@@ -324,6 +353,71 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #endif
     __syncwarp();
 
+    // Coupling product for complex-structured G (CPLX): with n = N/2 real
+    // spins first, G = [[R, -I], [I, R]] and B = -Ks G,
+    //   D_re = X + Y, D_im = Z - X + Y,  X = W_re (-Ks R), Y = W_im (-Ks I),
+    //   Z = (W_re + W_im)(-Ks (R - I)),
+    // 3 products of K = N/2 (18 HMMA at N = 32) instead of 4 (24 HMMA).
+    [[maybe_unused]] auto cplx_product = [&](const float2 (&w)[2][NT], float (&acc)[NT][4]) {
+                // D_re = X + Y, D_im = Z - X + Y with X = V_re (-Ks R), Y = V_im (-Ks I),
+                // Z = (V_re + V_im)(-Ks (R - I)): 3 products of K = N/2 instead of 4
+                constexpr int KH = KT / 2, NH = NT / 2;
+                auto afrag = [&](int kt, int off, uint32_t (&ahi)[4], uint32_t (&alo)[4]) {
+                    // k-tile kt of the half starting at n-tile off; off < 0: the sum
+                    if (off >= 0) {
+                        split_h2(w[0][off + 2 * kt], ahi[0], alo[0]);
+                        split_h2(w[1][off + 2 * kt], ahi[1], alo[1]);
+                        split_h2(w[0][off + 2 * kt + 1], ahi[2], alo[2]);
+                        split_h2(w[1][off + 2 * kt + 1], ahi[3], alo[3]);
+                    } else {
+                        split_h2(__fadd2_rn(w[0][2 * kt], w[0][NH + 2 * kt]), ahi[0], alo[0]);
+                        split_h2(__fadd2_rn(w[1][2 * kt], w[1][NH + 2 * kt]), ahi[1], alo[1]);
+                        split_h2(__fadd2_rn(w[0][2 * kt + 1], w[0][NH + 2 * kt + 1]), ahi[2], alo[2]);
+                        split_h2(__fadd2_rn(w[1][2 * kt + 1], w[1][NH + 2 * kt + 1]), ahi[3], alo[3]);
+                    }
+                };
+                auto mma3 = [&](float (&d)[4], const uint32_t (&ahi)[4], const uint32_t (&alo)[4],
+                                const uint4 f) {
+                    if (SPLIT) {
+                        mma_f16(d, alo, f.x, f.y);
+                        mma_f16(d, ahi, f.z, f.w);
+                    }
+                    mma_f16(d, ahi, f.x, f.y);
+                };
+                // Y into the real-half accumulators
+#pragma unroll
+                for (int kt = 0; kt < KH; ++kt) {
+                    uint32_t ahi[4], alo[4];
+                    afrag(kt, NH, ahi, alo);
+#pragma unroll
+                    for (int n = 0; n < NH; ++n) mma3(acc[n], ahi, alo, frag[((kt + KH) * NT + n) * 32 + lane]);
+                }
+                // copy Y to the imaginary half, then X on top of Y (real half)
+#pragma unroll
+                for (int n = 0; n < NH; ++n)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[n + NH][q] = acc[n][q];
+#pragma unroll
+                for (int kt = 0; kt < KH; ++kt) {
+                    uint32_t ahi[4], alo[4];
+                    afrag(kt, 0, ahi, alo);
+#pragma unroll
+                    for (int n = 0; n < NH; ++n) mma3(acc[n], ahi, alo, frag[(kt * NT + n) * 32 + lane]);
+                }
+                // imaginary half: Y - X = 2 Y - (X + Y), then + Z
+#pragma unroll
+                for (int n = 0; n < NH; ++n)
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) acc[n + NH][q] = fmaf(2.f, acc[n + NH][q], -acc[n][q]);
+#pragma unroll
+                for (int kt = 0; kt < KH; ++kt) {
+                    uint32_t ahi[4], alo[4];
+                    afrag(kt, -1, ahi, alo);
+#pragma unroll
+                    for (int n = 0; n < NH; ++n)
+                        mma3(acc[n + NH], ahi, alo, frag[(kt * NT + n + NH) * 32 + lane]);
+                }
+    };
     int until_refresh = 0;
     for (int step = 0; step < s.n_steps; ++step) {
         if (until_refresh == 0) {
@@ -405,6 +499,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 }
             }
 #else
+            if constexpr (CPLX) {
+                cplx_product(v, acc);
+            } else {
 #pragma unroll
             for (int kt = 0; kt < KT; ++kt) {
                 // A fragment: a0 = (g, 2t..), a1 = (g+8, 2t..), a2 = (g, 2t+8..), a3 = (g+8, 2t+8..)
@@ -431,6 +528,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                     }
                     mma_f16(acc[n], ahi, f.x, f.y);
                 }
+            }
             }
 #endif
 #if IL_FUSE_Q
@@ -660,18 +758,24 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         float acc[NT][4];
 #pragma unroll
         for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+        // (CPLX: the staged tiles are the 3-product ones; u is exact in f16, so
+        // its lo part is zero and the product has the same error bound)
+        if constexpr (CPLX) {
+            cplx_product(u, acc);
+        } else {
 #pragma unroll
-        for (int kt = 0; kt < KT; ++kt) {
-            uint32_t a[4];
-            a[0] = h2_bits(__float22half2_rn(u[0][2 * kt]));
-            a[1] = h2_bits(__float22half2_rn(u[1][2 * kt]));
-            a[2] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[0][2 * kt + 1])) : 0u;
-            a[3] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[1][2 * kt + 1])) : 0u;
+            for (int kt = 0; kt < KT; ++kt) {
+                uint32_t a[4];
+                a[0] = h2_bits(__float22half2_rn(u[0][2 * kt]));
+                a[1] = h2_bits(__float22half2_rn(u[1][2 * kt]));
+                a[2] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[0][2 * kt + 1])) : 0u;
+                a[3] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[1][2 * kt + 1])) : 0u;
 #pragma unroll
-            for (int n = 0; n < NT; ++n) {
-                const uint4 f = frag[(kt * NT + n) * 32 + lane];
-                mma_f16(acc[n], a, f.z, f.w);
-                mma_f16(acc[n], a, f.x, f.y);
+                for (int n = 0; n < NT; ++n) {
+                    const uint4 f = frag[(kt * NT + n) * 32 + lane];
+                    mma_f16(acc[n], a, f.z, f.w);
+                    mma_f16(acc[n], a, f.x, f.y);
+                }
             }
         }
         // unscaled FP32-screen energies (without -2 tr G) of rows g, g+8
@@ -802,7 +906,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     }
 }
 
-template <int NT, bool SPLIT, bool SAME_QR>
+template <int NT, bool SPLIT, bool SAME_QR, bool CPLX = false>
 int launch_cfg(const double* G, const double* g, const double* b, const uint64_t* base_seed,
                const double* eps_p, int64_t n_tasks, int tiles, const FastScalars& fs,
                int8_t* spins, uint8_t* diverged, double* energies, bool screened,
@@ -817,7 +921,7 @@ int launch_cfg(const double* G, const double* g, const double* b, const uint64_t
         f2.n_slots = std::max<int>(f2.n_slots, (int)(t1 / tiles - t0 / tiles + 1));
     }
     const size_t smem = FastLayout<NT>::smem(f2.n_slots);
-    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR>;
+    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR, CPLX>;
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     IL_LAUNCH(kProfAnneal, st, fn<<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(G, g, b, base_seed, eps_p, n_tasks, tiles,
@@ -830,9 +934,19 @@ template <int NT>
 int launch_nt(const double* G, const double* g, const double* b, const uint64_t* base_seed,
               const double* eps_p, int64_t P, int B, const FastScalars& fs, bool split,
               bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, bool screened,
-              cudaStream_t st) {
+              bool cplx, cudaStream_t st) {
     const int tiles = B / 16;
     const int64_t n_tasks = P * tiles;
+    // complex-structured G (every Ising built from a complex Gram): the
+    // 3-product refresh, for n = N/2 a multiple of 16 (real / imaginary spins
+    // on whole k-tiles) at the default operating point
+    if constexpr ((NT == 4 || NT == 8) && IL_CPLX_MVM) {
+        if (cplx && same_qr)
+            return split ? launch_cfg<NT, true, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                            spins, diverged, energies, screened, st)
+                         : launch_cfg<NT, false, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles,
+                                                             fs, spins, diverged, energies, screened, st);
+    }
     if (split) {
         return same_qr ? launch_cfg<NT, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
                                                    spins, diverged, energies, screened, st)
@@ -875,7 +989,7 @@ bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st, int screen_rows) {
+                       double* energies, cudaStream_t st, int screen_rows, bool cplx) {
     if (!fast_anneal_supported(N, B, s)) {
         set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
         return IL_ERR_UNSUPPORTED;
@@ -918,7 +1032,7 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
         return launch_anneal_umma(G, g, b, base_seed, eps_p, P, N, B, &fs, split, same_qr, spins,
                                   diverged, energies, screened, st);
 #define IL_NT(k) \
-    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, st)
+    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, cplx, st)
     switch (N / 8) {
         IL_NT(1);
         IL_NT(2);
