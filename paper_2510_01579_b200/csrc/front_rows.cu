@@ -35,6 +35,9 @@ constexpr int kGramUnroll = IL_GRAM_UNROLL;
 #ifndef IL_PROBE_NO_LAMBDA
 #define IL_PROBE_NO_LAMBDA 0
 #endif
+#ifndef IL_FRONT_TMA  // H, y staged by TMA bulk copies
+#define IL_FRONT_TMA 0  // measured slower: 0.80 -> 1.22 ms per 16x16 slot
+#endif
 #ifndef IL_FRONT_SAVE_A  // phase 1 reloads the Gram rows instead of recomputing them
 #define IL_FRONT_SAVE_A 1
 #endif
@@ -242,10 +245,29 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
     uint8_t* idx = x_idx + prob * 2 * n;
     {
         const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n;
-        for (int i = r; i < n_r * n; i += GS) H[i] = Hp[i];
         const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
+#if IL_FRONT_TMA
+        // H and y by 1-D TMA bulk copies (one lane of the group issues, every
+        // lane waits on the group's mbarrier): no per-lane load loop whose
+        // iterations each wait out a DRAM round trip
+        __shared__ __align__(8) uint64_t bars[kRowsThreads / GS];
+        uint64_t* bar = &bars[grp];
+        if (r == 0) {
+            mbar_init(bar, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            const uint32_t hb = (uint32_t)(sizeof(cplx) * n_r * n), yb = (uint32_t)(sizeof(cplx) * n_r);
+            mbar_expect_tx(bar, hb + yb);
+            tma_bulk_g2s(H, Hp, hb, bar);
+            tma_bulk_g2s(y, yp, yb, bar);
+        }
+        vb[GS + r] = wb[GS + r] = cplx{0.0, 0.0};  // zero tails read by shifted columns
+        g.sync();
+        mbar_wait(bar, 0);
+#else
+        for (int i = r; i < n_r * n; i += GS) H[i] = Hp[i];
         for (int i = r; i < n_r; i += GS) y[i] = yp[i];
         vb[GS + r] = wb[GS + r] = cplx{0.0, 0.0};  // zero tails read by shifted columns
+#endif
     }
     g.sync();
     const double c = 0.5 * al.spacing;
