@@ -279,6 +279,28 @@ def test_fast_kernel_any_replica_count(n_anneals):
         assert np.array_equal(ex.x_idx[i].cpu().numpy(), want)
 
 
+@pytest.mark.parametrize("kw", [dict(), dict(p=1.2, a=0.3), dict(zeta=0.8),
+                                dict(diverge_threshold=0.9), dict(dt=0.01, n_steps=256)])
+def test_fast_kernel_operating_points(kw):
+    """The FP32 kernel's instantiations: the scaled state at the reference
+    operating point (x- and e-factors equal), the general path when they
+    differ (p - 1 != zeta a, zeta != 1), tight divergence thresholds and a
+    finer step -- each against the bit-exact FP64 kernel on the fixture REs."""
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    d = load_golden("d16x16_16qam_20db.npz")
+    args = (d["H"], d["y"], d["noise_var"], int(d["order"]), d["seed"])
+    ex = batched.detect_cim_batch(*args, CacParams(precision="fp64_exact", **kw))
+    fa = batched.detect_cim_batch(*args, CacParams(precision="fp32", **kw))
+    e_ex, e_fa = ex.energy.cpu().numpy(), fa.energy.cpu().numpy()
+    assert (e_fa <= e_ex * (1 + 1e-12)).mean() >= 0.99, kw
+    same = np.all(fa.x_idx.cpu().numpy() == ex.x_idx.cpu().numpy(), axis=(1, 2)).mean()
+    assert same >= 0.97, (kw, same)
+    # divergence counts agree (the scaled path tests q = alpha - dt x^2)
+    dex, dfa = ex.diverged.cpu().numpy(), fa.diverged.cpu().numpy()
+    assert np.abs(dex - dfa).mean() <= 0.5, kw
+
+
 @pytest.mark.parametrize("n_chunks", [0, 1, 4])
 def test_precode_vpp_host_pipeline_matches_device_batch(n_chunks):
     from paper_2510_01579_b200 import batched
