@@ -63,6 +63,38 @@ __device__ void gram_hermitian(const cplx* H, const cplx* y, int n_r, int n_t, c
 // lane i owns row i); inv_diag[k] = 1 / L[k][k] (scaling by the reciprocal,
 // as LAPACK's zpotrf does).  Returns false on a non-positive pivot (the
 // reference raises LinAlgError from cho_factor in that case).
+template <unsigned GMASK_ALL = 0>
+__device__ bool cholesky_lower_g(cplx* M, int n, double* inv_diag, int lane, unsigned mask) {
+    // lane: index within the group that owns M; mask: the group's warp lanes
+    for (int k = 0; k < n; ++k) {
+        const double piv = M[k * n + k].re;
+        if (!(piv > 0.0)) return false;
+        const double lkk = sqrt(piv);
+        const double inv = 1.0 / lkk;
+        __syncwarp(mask);
+        cplx lik = {0.0, 0.0};
+        if (lane > k && lane < n) {
+            const cplx v = M[lane * n + k];
+            lik = {v.re * inv, v.im * inv};
+            M[lane * n + k] = lik;
+        }
+        if (lane == k) {
+            M[k * n + k] = {lkk, 0.0};
+            inv_diag[k] = inv;
+        }
+        __syncwarp(mask);
+        if (lane > k && lane < n) {
+            for (int j = k + 1; j <= lane; ++j) {
+                const cplx ljk = M[j * n + k];
+                M[lane * n + j].re -= lik.re * ljk.re + lik.im * ljk.im;
+                M[lane * n + j].im -= lik.im * ljk.re - lik.re * ljk.im;
+            }
+        }
+        __syncwarp(mask);
+    }
+    return true;
+}
+
 __device__ bool cholesky_lower(cplx* M, int n, double* inv_diag, int lane) {
     for (int k = 0; k < n; ++k) {
         const double piv = M[k * n + k].re;
@@ -503,25 +535,34 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
 // ---------------------------------------------------------------------------
 // ZF / VPP front-end (precoder.py:54-60, 93-125)
 // ---------------------------------------------------------------------------
+#ifndef IL_VPP_GROUPS  // 8-lane groups (4 problems per warp) for n_u, n_ant <= 8
+#define IL_VPP_GROUPS 1
+#endif
+// GS lanes per problem (32: one warp; 8: four problems per warp when n_u and
+// n_ant are <= 8); every element is computed by one lane with the same
+// sequence of operations whichever GS, and the group sums add the same
+// nonzero terms in the same tree order, so the outputs are bit-identical.
+template <int GS>
 __global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __restrict__ ug,
                                int64_t P, int n_u, int n_ant, double tau, double* __restrict__ Wg,
                                double* __restrict__ ytg, double* __restrict__ Hpg,
                                double* __restrict__ base_energy, int8_t* __restrict__ status) {
     extern __shared__ __align__(16) char smem_raw[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
-    if (prob >= P) return;
+    const int lane = threadIdx.x & (GS - 1), warp = threadIdx.x / GS;  // group lane, group
+    const unsigned mask = GS == 32 ? kFull : (((1u << GS) - 1u) << ((threadIdx.x & 31) & ~(GS - 1)));
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x / GS) + warp;
+    if (prob >= P) return;  // whole groups exit together
     const size_t per_warp = sizeof(cplx) * ((size_t)n_u * n_ant * 2 + (size_t)n_u * n_u + n_u);
     cplx* H = reinterpret_cast<cplx*>(smem_raw + warp * per_warp);  // [n_u x n_ant]
     cplx* X = H + n_u * n_ant;                                      // [n_u x n_ant]
     cplx* L = X + n_u * n_ant;                                      // [n_u x n_u]
     cplx* u = L + n_u * n_u;
     const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_u * n_ant;
-    for (int i = lane; i < n_u * n_ant; i += 32) H[i] = X[i] = Hp[i];
-    for (int i = lane; i < n_u; i += 32) u[i] = reinterpret_cast<const cplx*>(ug)[prob * n_u + i];
-    __syncwarp();
+    for (int i = lane; i < n_u * n_ant; i += GS) H[i] = X[i] = Hp[i];
+    for (int i = lane; i < n_u; i += GS) u[i] = reinterpret_cast<const cplx*>(ug)[prob * n_u + i];
+    __syncwarp(mask);
     // A = H H^H  (row i of H against row j)
-    for (int idx = lane; idx < n_u * n_u; idx += 32) {
+    for (int idx = lane; idx < n_u * n_u; idx += GS) {
         const int i = idx / n_u, j = idx % n_u;
         if (i > j) continue;
         double re = 0.0, im = 0.0;
@@ -534,13 +575,14 @@ __global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __re
         L[i * n_u + j] = {re, im};
         L[j * n_u + i] = {re, -im};
     }
-    __syncwarp();
-    __shared__ double invd_all[8][32];
+    __syncwarp(mask);
+    __shared__ double invd_all[32][32];
     double* invd = invd_all[warp];
-    const bool ok = cholesky_lower(L, n_u, invd, lane);
+    const bool ok = GS == 32 ? cholesky_lower(L, n_u, invd, lane)
+                             : cholesky_lower_g(L, n_u, invd, lane, mask);
     if (lane == 0 && status) status[prob] = ok ? 0 : -1;
     // X = A^-1 H, one column per lane
-    for (int col = lane; col < n_ant; col += 32) {
+    for (int col = lane; col < n_ant; col += GS) {
         if (!ok) break;
         for (int k = 0; k < n_u; ++k) {
             const double lkk = L[k * n_u + k].re;
@@ -555,12 +597,12 @@ __global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __re
             X[k * n_ant + col] = {acc.re / lkk, acc.im / lkk};
         }
     }
-    __syncwarp();
+    __syncwarp(mask);
     // W = X^H [n_ant x n_u]; y_t = W u; H_p = -tau/2 W
     cplx* W = reinterpret_cast<cplx*>(Wg) + prob * (int64_t)n_ant * n_u;
     cplx* Hq = reinterpret_cast<cplx*>(Hpg) + prob * (int64_t)n_ant * n_u;
     const double ht = -tau / 2.0;
-    for (int idx = lane; idx < n_ant * n_u; idx += 32) {
+    for (int idx = lane; idx < n_ant * n_u; idx += GS) {
         const int a = idx / n_u, i = idx % n_u;
         const cplx xv = X[i * n_ant + a];
         const cplx wv = {xv.re, -xv.im};
@@ -569,7 +611,7 @@ __global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __re
     }
     double acc = 0.0;
     cplx* yt = reinterpret_cast<cplx*>(ytg) + prob * (int64_t)n_ant;
-    for (int a = lane; a < n_ant; a += 32) {
+    for (int a = lane; a < n_ant; a += GS) {
         cplx s = {0.0, 0.0};
         for (int i = 0; i < n_u; ++i) {
             const cplx xv = X[i * n_ant + a];
@@ -578,7 +620,12 @@ __global__ void k_zf_vpp_front(const double* __restrict__ Hg, const double* __re
         yt[a] = s;
         acc += cabs2(s);
     }
-    acc = warp_sum(acc);
+    if constexpr (GS == 32) {
+        acc = warp_sum(acc);
+    } else {  // the nonzero levels of warp_sum's tree (lanes >= GS hold 0)
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(mask, acc, o, GS));
+    }
     if (lane == 0) base_energy[prob] = acc;
 }
 
@@ -770,13 +817,24 @@ int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, in
                         int8_t* status, cudaStream_t st) {
     if (P == 0) return IL_OK;
     const size_t per_warp = sizeof(cplx) * ((size_t)n_u * n_ant * 2 + (size_t)n_u * n_u + n_u);
+    if (n_u <= 8 && n_ant <= 8 && IL_VPP_GROUPS) {  // four problems per warp, 16 per block
+        constexpr int GS = 8, kGroups = 16;
+        const size_t smem = per_warp * kGroups;
+        int rc = set_smem((const void*)k_zf_vpp_front<GS>, smem);
+        if (rc) return rc;
+        const int blocks = (int)((P + kGroups - 1) / kGroups);
+        IL_LAUNCH(kProfFront, st, k_zf_vpp_front<GS><<<blocks, GS * kGroups, smem, st>>>(H, u, P, n_u, n_ant, tau, W, y_t, H_p,
+                                                       base_energy, status););
+        IL_CHECK_CUDA(cudaGetLastError());
+        return IL_OK;
+    }
     int wpb = (int)((200 * 1024) / per_warp);
     wpb = wpb < 1 ? 1 : (wpb > 4 ? 4 : wpb);
     const size_t smem = per_warp * wpb;
-    int rc = set_smem((const void*)k_zf_vpp_front, smem);
+    int rc = set_smem((const void*)k_zf_vpp_front<32>, smem);
     if (rc) return rc;
     const int blocks = (int)((P + wpb - 1) / wpb);
-    IL_LAUNCH(kProfFront, st, k_zf_vpp_front<<<blocks, 32 * wpb, smem, st>>>(H, u, P, n_u, n_ant, tau, W, y_t, H_p,
+    IL_LAUNCH(kProfFront, st, k_zf_vpp_front<32><<<blocks, 32 * wpb, smem, st>>>(H, u, P, n_u, n_ant, tau, W, y_t, H_p,
                                                    base_energy, status););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
