@@ -36,6 +36,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "il_internal.cuh"
@@ -83,6 +84,12 @@ constexpr int kWarpsPerCta = 4;
 #endif
 #ifndef IL_PROBE_NO_ENERGY  // timing probe only: skips the FP64 energies (wrong output)
 #define IL_PROBE_NO_ENERGY 0
+#endif
+#ifndef IL_SCREEN_PREFETCH  // N = 32: G column for the FP64 re-evaluation loaded early
+#define IL_SCREEN_PREFETCH 0  // measured within noise (+0.3%)
+#endif
+#ifndef IL_PROBE_CAND  // probe: print candidate / evaluation counts of sampled tiles
+#define IL_PROBE_CAND 0
 #endif
 #ifndef IL_PROBE_NO_RNG  // timing probe only: constant initial states (wrong output)
 #define IL_PROBE_NO_RNG 0
@@ -743,6 +750,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         dflag[h] = SC ? !(d >= s.qthr) : !(d <= s.thr2);
         if (t == 0) diverged[row] = dflag[h] ? 1 : 0;
     }
+#if IL_PROBE_NO_ENERGY
+    if (screened) {
+        if (t < 2) energies[row0 + g + 8 * t] = (double)(pos[t] ^ neg[t]);
+        return;
+    }
+#endif
     if (screened) {
         // Selection screen: E + 2 tr G in FP32 from the tensor cores.  u =
         // s_A + s_B in {-2, 0, 2} is exact in f16, so two passes over the
@@ -755,6 +768,16 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             for (int n = 0; n < NT; ++n)
                 u[h][n] = make_float2((xA[h][n].x >= 0.f ? 1.f : -1.f) + (xB[h][n].x >= 0.f ? 1.f : -1.f),
                                       (xA[h][n].y >= 0.f ? 1.f : -1.f) + (xB[h][n].y >= 0.f ? 1.f : -1.f));
+        // N = 32: lane i's column of G (and G[i][i], b[i]) for the FP64
+        // re-evaluation, loaded now so the L2 round trip overlaps the screen
+        constexpr bool kPre = (N == 32) && IL_SCREEN_PREFETCH;
+        [[maybe_unused]] double gcol[kPre ? 32 : 1], gdiag = 0.0, bown = 0.0;
+        if constexpr (kPre) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) gcol[j] = L::kSmemG ? G[j * N + lane] : __ldg(G + j * N + lane);
+            gdiag = L::kSmemG ? G[lane * N + lane] : __ldg(G + lane * N + lane);
+            bown = bv_p[lane];
+        }
         float acc[NT][4];
 #pragma unroll
         for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
@@ -814,9 +837,19 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         double* w = reinterpret_cast<double*>(frag);  // fragments are consumed
         __syncwarp();
         double tr = 0.0;
-        for (int i = lane; i < N; i += 32) tr += G[(int64_t)i * N + i];
+        if constexpr (kPre) {
+            tr = gdiag;
+        } else {
+            for (int i = lane; i < N; i += 32) tr += G[(int64_t)i * N + i];
+        }
         tr = warp_sum(tr);
+#if IL_PROBE_CAND
+        int n_eval = 0, n_cand0 = __popc(cand);
+#endif
         while (cand) {
+#if IL_PROBE_CAND
+            ++n_eval;
+#endif
             const int l = __ffs(cand) - 1;
             const uint64_t cp = __shfl_sync(0xffffffffu, my_pos, l);
             const uint64_t cn = __shfl_sync(0xffffffffu, my_neg, l);
@@ -827,6 +860,15 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 w[j] = (double)((int)((cp >> j) & 1u) - (int)((cn >> j) & 1u));
             __syncwarp();
             double q = 0.0, li = 0.0;
+            if constexpr (kPre) {  // same operations and order as the loop below
+                double gu[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) gu[r] = fma(gcol[j + r], w[j + r], gu[r]);
+                q = fma(w[lane], (gu[0] + gu[1]) + (gu[2] + gu[3]), q);
+                li = fma(bown, w[lane], li);
+            } else {
             for (int i = lane; i < N; i += 32) {
                 double gu[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -838,6 +880,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 q = fma(w[i], (gu[0] + gu[1]) + (gu[2] + gu[3]), q);
                 li = fma(bv_p[i], w[i], li);
             }
+            }
             __syncwarp();
             q = warp_sum(q);
             li = warp_sum(li);
@@ -848,6 +891,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             cand &= ~__ballot_sync(0xffffffffu, same);
         }
         if (t < 2) energies[row0 + g + 8 * t] = my_e;
+#if IL_PROBE_CAND
+        if (lane == 0 && (blockIdx.x % 512) == 0)
+            printf("cand %d eval %d\n", n_cand0, n_eval);
+#endif
         return;
     }
     // FP64 energies.  Row sums use G's symmetry: sum_j s_j G[j][i] reads row j
