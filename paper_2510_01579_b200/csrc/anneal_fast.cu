@@ -8,28 +8,33 @@
 //
 // Mapping (one warp = 16 anneals of one problem, N = 8*NT spins per half):
 //   The refresh is the small GEMM  M^T[a][i] = sum_j V^T[a][j] G[j][i]  with
-//   a = anneal (MMA M dimension), i = spin (N dimension), j = spin (K).  It is
-//   issued as mma.sync.m16n8k8 TF32 tiles.  Thread (g = lane/4, t = lane%4)
-//   owns anneals {g, g+8} and, in every n-tile n, spins {8n+2t, 8n+2t+1} of
-//   both halves: exactly the accumulator (C) fragment of the tile.  The A
-//   fragment of k-tile k wants columns {t, t+4}; ordering the K dimension of
-//   tile k as (8k+0, 8k+2, 8k+4, 8k+6, 8k+1, 8k+3, 8k+5, 8k+7) makes those
-//   columns spins {8k+2t, 8k+2t+1} -- the thread's own.  G's B fragments are
-//   staged once per problem in that permuted order, so a refresh moves no
-//   data between lanes at all: v = x1 + x2 is formed in registers, fed to
+//   a = anneal (MMA M dimension), i = spin (N dimension), j = spin (K), issued
+//   as mma.sync.m16n8k16 f16 tiles with FP32 accumulate.  Thread (g = lane/4,
+//   t = lane%4) owns anneals {g, g+8} and, in every n-tile n, spins {8n+2t,
+//   8n+2t+1} of both halves: exactly the accumulator (C) fragment of the tile.
+//   The A fragment of k-tile k wants the thread's columns {2t, 2t+1, 2t+8,
+//   2t+9}; ordering K inside the tile so that those are spins {16k+2t, +1}
+//   and {16k+8+2t, +1} (n-tiles 2k and 2k+1) makes them the thread's own.
+//   G's B fragments are staged once per problem in that order, so a refresh
+//   moves no data between lanes: v = x1 + x2 is formed in registers, fed to
 //   the MMA, and the result lands where the Euler update needs it.
-//   IL_PREC_FP32 splits both operands into TF32 hi + lo parts (3 MMAs per
-//   tile: hi*hi + lo*hi + hi*lo), giving FP32-level accuracy; IL_PREC_TF32
-//   uses one pass.
-//   The Euler update runs on packed FP32x2 (FFMA2/FMUL2) over spin pairs.
-//   The aux spin (one per anneal) is integrated redundantly and bit-identically
-//   by the 4 lanes of a quad; c_aux comes from a quad shuffle reduction.
+//   IL_PREC_FP32 splits both operands into f16 hi + lo parts (3 MMAs per
+//   tile: hi*hi + lo*hi + hi*lo) for FP32-level accuracy; IL_PREC_TF32 uses
+//   one pass.  The Euler update runs on packed FP32x2 (FFMA2/FMUL2) over spin
+//   pairs; at the reference operating point the state is stored as sqrt(dt) x
+//   (IL_SCALED_X) so that the update is 4 packed ops per pair.  The aux spin
+//   (one per anneal) is integrated redundantly and bit-identically by the 4
+//   lanes of a quad; c_aux comes from a quad shuffle reduction.
 //
-// Divergence: a per-anneal sticky max of x^2 (NaN-propagating), which yields
-// exactly the reference's `diverged` flag; spins of a diverged anneal are not
-// frozen at the halting step, which is harmless because diverged anneals are
-// excluded from selection (solver.py:262-264).  The exact kernel serves the
-// drop-in run_anneals path where frozen spins are part of the contract.
+// Divergence: a per-anneal sticky NaN-propagating extremum (max of x^2, or
+// the min of the scaled factor q), matching the reference's `diverged` flag;
+// spins of a diverged anneal are not frozen at the halting step, which is
+// harmless because diverged anneals are excluded from selection
+// (solver.py:262-264).  The exact kernel serves the drop-in run_anneals path
+// where frozen spins are part of the contract.
+//
+// Energies: every anneal's in FP64, or (the detection path) an FP32
+// tensor-core screen with FP64 for the anneals that can be the argmin.
 //
 // Scaling: G, g, b are pre-multiplied by -dt*eps so that the MMA directly
 // yields the -dt*eps*c term of the update.
