@@ -12,12 +12,12 @@
 //   as mma.sync.m16n8k16 f16 tiles with FP32 accumulate.  Thread (g = lane/4,
 //   t = lane%4) owns anneals {g, g+8} and, in every n-tile n, spins {8n+2t,
 //   8n+2t+1} of both halves: exactly the accumulator (C) fragment of the tile.
-//   The A fragment of k-tile k wants the thread's columns {2t, 2t+1, 2t+8,
-//   2t+9}; ordering K inside the tile so that those are spins {16k+2t, +1}
-//   and {16k+8+2t, +1} (n-tiles 2k and 2k+1) makes them the thread's own.
-//   G's B fragments are staged once per problem in that order, so a refresh
-//   moves no data between lanes: v = x1 + x2 is formed in registers, fed to
-//   the MMA, and the result lands where the Euler update needs it.
+//   The A fragment of k-tile k holds the thread's columns {2t, 2t+1, 2t+8,
+//   2t+9}, i.e. spins {16k+2t, +1} and {16k+8+2t, +1}: n-tiles 2k and 2k+1 of
+//   the thread's own spins.  G's B fragments are staged once per problem, so
+//   a refresh moves no data between lanes: v = x1 + x2 is formed in
+//   registers, fed to the MMA, and the result lands where the Euler update
+//   needs it.
 //   IL_PREC_FP32 splits both operands into f16 hi + lo parts (3 MMAs per
 //   tile: hi*hi + lo*hi + hi*lo) for FP32-level accuracy; IL_PREC_TF32 uses
 //   one pass.  The Euler update runs on packed FP32x2 (FFMA2/FMUL2) over spin
