@@ -2,7 +2,8 @@
 only for the anneals that can be the argmin) must not change any output of
 the detection path: compare it against the all-FP64 epilogue
 (ISINGLINK_SCREEN=0, read once per process -> subprocess) bit for bit, over
-SNRs from noisy (many near-ties between anneal energies) to clean."""
+SNRs from noisy (many near-ties between anneal energies) to clean, and every
+spin count the screen serves (N = 24, 32, 48, 64)."""
 import json
 import os
 import subprocess
@@ -21,7 +22,7 @@ from paper_2510_01579_b200 import batched
 from paper_2510_01579_b200.params import CacParams
 out = {{}}
 for n_t, order, snr, P in ((16, 16, 5.0, 3000), (16, 16, 20.0, 3000), (12, 64, 25.0, 2000),
-                           (16, 4, 0.0, 2000)):
+                           (16, 4, 0.0, 2000), (24, 16, 20.0, 600), (32, 4, 10.0, 400)):
     H, y, nv, seeds, _ = batch(n_t, order, snr, P, 11 + n_t)
     for prec in ("fp32", "tf32"):
         r = batched.detect_cim_batch(H, y, nv, order, seeds, CacParams(precision=prec))
