@@ -301,6 +301,24 @@ def test_fast_kernel_operating_points(kw):
     assert np.abs(dex - dfa).mean() <= 0.5, kw
 
 
+@pytest.mark.parametrize("n_t,order", [(24, 16), (32, 4), (12, 16)])
+def test_fast_kernel_large_and_odd_spin_counts(n_t, order):
+    """N = 48 / 64 (k_front with a warp per RE, 6 / 8 n-tiles) and N = 24
+    (odd tile count, padded K) in FP32 against the bit-exact FP64 kernel."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from tools.parity_scale import batch
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    H, y, nv, seeds, _ = batch(n_t, order, 15.0, 256, 77 + n_t)
+    ex = batched.detect_cim_batch(H, y, nv, order, seeds, CacParams(precision="fp64_exact"))
+    fa = batched.detect_cim_batch(H, y, nv, order, seeds, CacParams(precision="fp32"))
+    e_ex, e_fa = ex.energy.cpu().numpy(), fa.energy.cpu().numpy()
+    assert (e_fa <= e_ex * (1 + 1e-12)).mean() >= 0.98
+    same = (fa.x_idx == ex.x_idx).all(-1).all(-1).float().mean().item()
+    assert same >= 0.95, same
+
+
 @pytest.mark.parametrize("n_chunks", [0, 1, 4])
 def test_precode_vpp_host_pipeline_matches_device_batch(n_chunks):
     from paper_2510_01579_b200 import batched
