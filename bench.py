@@ -502,6 +502,15 @@ def run_ours(args) -> None:
         diverged=torch.empty(P, dtype=torch.int32).pin_memory())]
     e2e_step()
     e2e_sync_ms = e2e_timed(False)
+    # untimed warm-up of the streamed path (its workspaces are sized for the
+    # two-chunk mode a slot takes while the previous one is still running)
+    prev = None
+    for k in range(max(args.warmup, 3)):
+        tk = batched.detect_cim_host_submit(Hh, yh, nvh, ORDER, sh, prm, out=outs[k % 2])
+        if prev is not None:
+            finish(prev.wait())
+        prev = tk
+    finish(prev.wait())
     e2e_ms = e2e_timed(True)
     e2e_value = P_all * args.steps / (e2e_ms / 1e3)
     e2e_sync_value = P_all * args.steps / (e2e_sync_ms / 1e3)
