@@ -23,6 +23,9 @@ using namespace il;
 #ifndef IL_PIPE_CAP_DIV
 #define IL_PIPE_CAP_DIV 8
 #endif
+#ifndef IL_POOL_RESERVE_MB  // memory-pool reserve for streamed slots
+#define IL_POOL_RESERVE_MB 6144
+#endif
 #ifndef IL_PIPE_TAPER  // halve the last chunks (env ISINGLINK_PIPE_TAPER=2 on, 1 off)
 #define IL_PIPE_TAPER 0
 #endif
@@ -71,6 +74,19 @@ void keep_pool_warm() {
         // with slots in flight on several streams that serialises them
         int no = 0;
         cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
+        // ... and reserve its working set once (freed, kept by the threshold
+        // above), so that no call has to grow the pool: growth blocks the
+        // enqueueing thread for milliseconds (measured 10-100 ms stalls)
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const size_t reserve = std::min<size_t>((size_t)IL_POOL_RESERVE_MB << 20, free_b / 4);
+            void* p = nullptr;
+            if (reserve && cudaMallocAsync(&p, reserve, 0) == cudaSuccess) {
+                cudaFreeAsync(p, 0);
+                cudaStreamSynchronize(0);
+            }
+            cudaGetLastError();
+        }
     }
     done = true;
 }
