@@ -22,6 +22,7 @@
 
 #include "il_group.cuh"
 #include "il_internal.cuh"
+#include "rng_numpy.cuh"
 
 namespace il {
 
@@ -34,6 +35,9 @@ constexpr int kRowsThreads = 128;
 constexpr int kGramUnroll = IL_GRAM_UNROLL;
 #ifndef IL_PROBE_NO_LAMBDA
 #define IL_PROBE_NO_LAMBDA 0
+#endif
+#ifndef IL_PROBE_FRONT_RNG
+#define IL_PROBE_FRONT_RNG 0
 #endif
 #ifndef IL_FRONT_TMA  // H, y staged by TMA bulk copies
 #define IL_FRONT_TMA 0  // measured slower: 0.80 -> 1.22 ms per 16x16 slot
@@ -427,6 +431,20 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
             o.b[prob * N + n + r] = -c * im;
         }
         if (o.offset && r == 0) o.offset[prob] = r2 + 2.0 * tr;
+#if IL_PROBE_FRONT_RNG
+        // timing probe only: the x0 replay of the anneal kernel (32 anneals x
+        // 2n+1... here 65 draws each, 2 per lane-anneal chain) done here
+        // instead; written over G (wrong results)
+        {
+            constexpr int kS = 65;
+            for (int a = r; a < 32; a += GS) {
+                Pcg64 rng;
+                rng.seed_from(derive_seed2((uint64_t)prob * 977u, (uint64_t)a));
+                float* dst = reinterpret_cast<float*>(o.G + prob * (int64_t)N * N) + a * kS;
+                for (int i = 0; i < kS; ++i) dst[i] = (float)rng.uniform(-0.1, 0.2);
+            }
+        }
+#endif
     }
 }
 
