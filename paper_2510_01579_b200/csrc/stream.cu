@@ -23,6 +23,9 @@ using namespace il;
 #ifndef IL_PIPE_CAP_DIV
 #define IL_PIPE_CAP_DIV 8
 #endif
+#ifndef IL_PIPE_IDLE_CHUNKS
+#define IL_PIPE_IDLE_CHUNKS 12
+#endif
 #ifndef IL_POOL_RESERVE_MB  // memory-pool reserve for streamed slots
 #define IL_POOL_RESERVE_MB 6144
 #endif
@@ -165,6 +168,10 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
     // chunks suffice and cost no ramp (5.12 vs 5.28 ms per 16x16 slot).
     if (n_chunks <= 0 && P >= 4096 && ss.tail && cudaEventQuery(ss.tail) == cudaErrorNotReady)
         n_chunks = 2;
+    // an idle device: IL_PIPE_IDLE_CHUNKS equal chunks (12: 5.75 ms per 16x16
+    // slot against 5.82 for the ramp, `tools/one_slot_sweep.py`); 0 keeps the ramp
+    else if (n_chunks <= 0 && P >= 4096 && IL_PIPE_IDLE_CHUNKS > 0)
+        n_chunks = IL_PIPE_IDLE_CHUNKS;
     const std::vector<int64_t> bounds = chunk_bounds(P, n_chunks);
     const int K = (int)bounds.size() - 1;
     static const int n_comp = std::min(Streams::kMaxComp, env_int("ISINGLINK_PIPE_STREAMS", 2));
