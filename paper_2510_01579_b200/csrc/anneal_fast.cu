@@ -53,7 +53,10 @@ namespace il {
 namespace {
 using namespace fastk;
 
-constexpr int kWarpsPerCta = 4;
+#ifndef IL_FAST_WARPS  // warps per CTA (2 warps = one problem at 32 anneals)
+#define IL_FAST_WARPS 4
+#endif
+constexpr int kWarpsPerCta = IL_FAST_WARPS;
 #ifndef IL_SPLIT_ACC
 #define IL_SPLIT_ACC 0
 #endif
@@ -134,7 +137,8 @@ struct FastLayout {
 // leaves e*C unchanged, and e' = max(floor, e r) becomes
 // e_s' = max(floor * 2^-sc, e_s r) -- power-of-two scalings are exact.
 template <int NT, bool SPLIT, bool SAME_QR, bool CPLX>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, NT <= 2 ? IL_FAST_MINB2 : (NT <= 4 ? IL_FAST_MINB : 1))
+__global__ void __launch_bounds__(kWarpsPerCta * 32,
+                                  (NT <= 2 ? IL_FAST_MINB2 : (NT <= 4 ? IL_FAST_MINB : 1)) * 4 / kWarpsPerCta)
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
               const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
