@@ -93,6 +93,10 @@ constexpr int kWarpsPerCta = IL_FAST_WARPS;
 #ifndef IL_PROBE_NO_ENERGY  // timing probe only: skips the FP64 energies (wrong output)
 #define IL_PROBE_NO_ENERGY 0
 #endif
+#ifndef IL_STEP_UNROLL  // unroll factor of the step loop
+#define IL_STEP_UNROLL 2
+#endif
+constexpr int kStepUnroll = IL_STEP_UNROLL;
 #ifndef IL_GMAX_WIDE  // the prologue's G scan with every load in flight at once
 #define IL_GMAX_WIDE 0  // measured 0.5% slower (the scan latency is already hidden)
 #endif
@@ -467,6 +471,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 }
     };
     int until_refresh = 0;
+#pragma unroll kStepUnroll
     for (int step = 0; step < s.n_steps; ++step) {
         if (until_refresh == 0) {
             until_refresh = s.f_mvm;
