@@ -33,6 +33,10 @@ constexpr int kRowsThreads = 128;
 #define IL_GRAM_UNROLL 1
 #endif
 constexpr int kGramUnroll = IL_GRAM_UNROLL;
+#ifndef IL_ELIM_UNROLL  // unroll of the Householder / Gauss-Jordan step loops
+#define IL_ELIM_UNROLL 1
+#endif
+constexpr int kElimUnroll = IL_ELIM_UNROLL;
 #ifndef IL_PROBE_NO_LAMBDA
 #define IL_PROBE_NO_LAMBDA 0
 #endif
@@ -112,7 +116,7 @@ __device__ double lambda_max_rows(const Grp<GS>& g, cplx (&A)[GS], int n, cplx* 
                                   double* dsm, double* esm) {
     const int r = g.r;
     // Householder tridiagonalisation; at step k, A[j] holds column k + j.
-#pragma unroll 1
+#pragma unroll kElimUnroll
     for (int k = 0; k + 2 < n; ++k) {
         const cplx xi = (r > k && r < n) ? A[0] : cplx{0.0, 0.0};
         const double sig2 = g.sum(cabs2(xi));
@@ -357,7 +361,7 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
             cplx diag = {1.0, 0.0};
             // Gauss-Jordan: pivot row k broadcast through vb (row) and misc (rhs);
             // at step k, A[j] holds column k + j
-#pragma unroll 1
+#pragma unroll kElimUnroll
             for (int k = 0; k < n; ++k) {
                 if (r == k) {
 #pragma unroll
