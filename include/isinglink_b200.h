@@ -38,9 +38,11 @@ enum il_status {
 enum il_precision {
     IL_PREC_FP64_EXACT = 0, /* FP64, reference evaluation order, no FMA contraction:
                                bit-identical to the reference "ext" kernel */
-    IL_PREC_FP32 = 1,       /* FP32 state, coupling product on tensor cores with
-                               3xTF32 split (FP32-accurate); the throughput mode */
-    IL_PREC_TF32 = 2        /* FP32 state, single-pass TF32 coupling product */
+    IL_PREC_FP32 = 1,       /* FP32 state, coupling product on tensor cores as a
+                               3-pass f16 hi/lo split (hi*hi + lo*hi + hi*lo, FP32
+                               accumulate; FP32-accurate); the throughput mode */
+    IL_PREC_TF32 = 2        /* FP32 state, single-pass f16 coupling product
+                               (11-bit significand, like TF32) */
 };
 
 /* Solver configuration — mirrors CacParams (solver.py:87-124). */

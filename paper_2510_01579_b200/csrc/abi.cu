@@ -141,7 +141,7 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
         energies = ws.get<double>((size_t)P * Bs, &rc);
         if (rc) return rc;
         rc = launch_anneal_fast(G, g, b, base, eps, P, N, Bs, s, prm->precision, spins, div,
-                                energies, st, /*screen_rows=*/B, /*cplx_structured=*/true);
+                                energies, st, /*screen_rows=*/B);
     } else {
         rc = launch_anneal_exact(G, g, b, nullptr, base, eps, P, N, B, s, spins, div, nullptr,
                                  nullptr, st);

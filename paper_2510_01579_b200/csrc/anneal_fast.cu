@@ -57,58 +57,17 @@ using namespace fastk;
 #define IL_FAST_WARPS 4
 #endif
 constexpr int kWarpsPerCta = IL_FAST_WARPS;
-#ifndef IL_SPLIT_ACC
-#define IL_SPLIT_ACC 0
-#endif
-#ifndef IL_FAST_MINB
+#ifndef IL_FAST_MINB  // CTAs per SM (4-warp CTAs) for 16 < N <= 32
 #define IL_FAST_MINB 3
 #endif
 #ifndef IL_FAST_MINB2  // CTAs per SM for N <= 16
 #define IL_FAST_MINB2 4
 #endif
-#ifndef IL_NOUTER  // MMA issue order: n-tile outer (early accumulators)
-#define IL_NOUTER 0
-#endif
-#ifndef IL_PB2  // packed partial sums for the aux coupling
-#define IL_PB2 1
-#endif
-#ifndef IL_TMA_G  // G, g, b of the CTA's problems staged in shared memory by TMA bulk copies
-#define IL_TMA_G 0  // measured 1% slower: the latency it hides was already covered
-#endif
-#ifndef IL_RNG2  // two interleaved PCG64 chains per lane for the initial states
-#define IL_RNG2 0  // measured 1% slower: the RNG is issue-bound, not latency-bound
-#endif
-#ifndef IL_KG_SMEM  // refresh constants Kg, -Kb in shared memory (frees 4 NT registers)
-#define IL_KG_SMEM 1
-#endif
-#ifndef IL_CPLX_MVM  // 3-product (Karatsuba) coupling refresh for complex-structured G
-#define IL_CPLX_MVM 0  // measured 1.7% slower (the extra FP32 work outweighs 6 HMMA)
-#endif
-#ifndef IL_EULER_GROUP  // Euler step issued stage by stage over groups of 4 spin pairs
-#define IL_EULER_GROUP 0  // measured within noise (16x16 -0.3%, 8x8 +0.9%)
-#endif
-#ifndef IL_FUSE_Q  // C-independent half of the first Euler step inside the refresh block
-#define IL_FUSE_Q 0  // measured 1.4% slower (register pressure; bit-identical)
-#endif
-#ifndef IL_PROBE_NO_ENERGY  // timing probe only: skips the FP64 energies (wrong output)
-#define IL_PROBE_NO_ENERGY 0
-#endif
 #ifndef IL_STEP_UNROLL  // unroll factor of the step loop
 #define IL_STEP_UNROLL 2
 #endif
 constexpr int kStepUnroll = IL_STEP_UNROLL;
-#ifndef IL_GMAX_WIDE  // the prologue's G scan with every load in flight at once
-#define IL_GMAX_WIDE 0  // measured 0.5% slower (the scan latency is already hidden)
-#endif
-#ifndef IL_SCREEN_PREFETCH  // N = 32: G column for the FP64 re-evaluation loaded early
-#define IL_SCREEN_PREFETCH 0  // measured within noise (+0.3%)
-#endif
-#ifndef IL_PROBE_CAND  // probe: print candidate / evaluation counts of sampled tiles
-#define IL_PROBE_CAND 0
-#endif
-#ifndef IL_PROBE_NO_RNG  // timing probe only: constant initial states (wrong output)
-#define IL_PROBE_NO_RNG 0
-#endif
+
 
 template <int NT>
 struct FastLayout {
@@ -118,18 +77,10 @@ struct FastLayout {
     static constexpr int kFragF4 = KT * NT * 32;          // uint4 per warp
     static constexpr int kX0F4 = (16 * S + 3) / 4;        // x0 staging, aliased
     // + one uint4 of per-warp scalars kept out of registers during the loop
-    // (IL_KG_SMEM) + NT x 32 uint4 of per-lane refresh constants {Kg, -Kb}
+    // + NT x 32 uint4 of per-lane refresh constants {Kg, -Kb}
     static constexpr int kKgF4 = (kFragF4 > kX0F4 ? kFragF4 : kX0F4) + 1;
-    static constexpr int kWarpF4 = kKgF4 + (IL_KG_SMEM ? NT * 32 : 0);
+    static constexpr int kWarpF4 = kKgF4 + NT * 32;
     static constexpr size_t kWarpBytes = sizeof(float4) * kWarpsPerCta * kWarpF4;
-    // IL_TMA_G: per staged problem G [N][N], g [N], b [N] in FP64, after the
-    // warps' fragment areas; one mbarrier per slot in front of everything
-    static constexpr bool kSmemG = IL_TMA_G && NT <= 4;
-    static constexpr size_t kSlotBytes = sizeof(double) * (N * N + 2 * N);
-    static constexpr size_t kBarBytes = 64;
-    static size_t smem(int n_slots) {
-        return kSmemG ? kBarBytes + kWarpBytes + kSlotBytes * n_slots : kWarpBytes;
-    }
 };
 
 // Tensor-core operand scaling.  The coupling product runs on f16 operands
@@ -140,7 +91,7 @@ struct FastLayout {
 // enters the update as e*C, so storing e_s = e * 2^-sc and C_s = C * 2^sc
 // leaves e*C unchanged, and e' = max(floor, e r) becomes
 // e_s' = max(floor * 2^-sc, e_s r) -- power-of-two scalings are exact.
-template <int NT, bool SPLIT, bool SAME_QR, bool CPLX>
+template <int NT, bool SPLIT, bool SAME_QR>
 __global__ void __launch_bounds__(kWarpsPerCta * 32,
                                   (NT <= 2 ? IL_FAST_MINB2 : (NT <= 4 ? IL_FAST_MINB : 1)) * 4 / kWarpsPerCta)
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
@@ -154,7 +105,6 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     constexpr int KT = L::KT;
     // scaled state (IL_SCALED_X): x~ = sqrt(dt) x wherever x is stored
     constexpr bool SC = IL_SCALED_X && SAME_QR;
-    static_assert(!(SC && (IL_FUSE_Q || IL_EULER_GROUP)), "variants assume the unscaled state");
     extern __shared__ __align__(16) uint4 smem_u4[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t task = (int64_t)blockIdx.x * kWarpsPerCta + warp;
@@ -165,123 +115,36 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     const int g = lane >> 2, t = lane & 3;
     const int hown = t & 1;  // the aux spin of anneal g + 8*hown is integrated by this lane
 
-    // ---- G, g, b: FP64 copies in shared memory (TMA) or straight from global
     const double* G = Gall + prob * (int64_t)N * N;
     const double* gv_p = gall + prob * N;
     const double* bv_p = ball + prob * N;
-    uint4* warp_area = smem_u4;
-    uint64_t* bar = nullptr;
-    if constexpr (L::kSmemG) {
-        // slot = problem index relative to the CTA's first problem; the first
-        // warp of each slot issues its bulk copies, every warp of the slot
-        // waits on the slot's mbarrier after generating its initial states
-        uint64_t* bars = reinterpret_cast<uint64_t*>(smem_u4);
-        warp_area = smem_u4 + L::kBarBytes / sizeof(uint4);
-        const int64_t first = (int64_t)blockIdx.x * kWarpsPerCta / tiles_per_prob;
-        const int slot = (int)(prob - first);
-        char* slots = reinterpret_cast<char*>(warp_area) + L::kWarpBytes;
-        if (threadIdx.x < s.n_slots) {
-            mbar_init(bars + threadIdx.x, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-        __syncthreads();
-        if (!valid) return;
-        bar = bars + slot;
-        const bool issuer = (warp == 0 || (task - 1) / tiles_per_prob != prob) && lane == 0;
-        double* Gs = reinterpret_cast<double*>(slots + L::kSlotBytes * slot);
-        if (issuer) {
-            mbar_expect_tx(bar, (uint32_t)L::kSlotBytes);
-            tma_bulk_g2s(Gs, G, sizeof(double) * N * N, bar);
-            tma_bulk_g2s(Gs + N * N, gv_p, sizeof(double) * N, bar);
-            tma_bulk_g2s(Gs + N * N + N, bv_p, sizeof(double) * N, bar);
-        }
-        G = Gs;
-        gv_p = Gs + N * N;
-        bv_p = Gs + N * N + N;
-    } else {
-        if (!valid) return;
-    }
-    uint4* frag = warp_area + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
-    float* x0s = reinterpret_cast<float*>(frag);      // x0 staging [16][S]
+    if (!valid) return;
+    uint4* frag = smem_u4 + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
+    float* x0s = reinterpret_cast<float*>(frag);    // x0 staging [16][S]
 
     // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
     {
         const int al = lane & 15, part = lane >> 4;
         const int a = mt * 16 + al;
-#if IL_PROBE_NO_RNG
-        for (int i = part; i < S; i += 2) x0s[al * S + i] = 0.01f * (float)((a * 7 + i * 13) % 19 - 9);
-        if (false) {
-#else
-        {
-#endif
         Pcg64 rng;
         rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)a));
-        if constexpr (IL_RNG2 && NT <= 4) {
-        // the stream is cut into 4 segments of Lseg draws; this lane runs
-        // segments 2 part and 2 part + 1 as two interleaved chains (jump-ahead)
-        constexpr int Lseg = (S + 3) / 4;
-        Pcg64 r2 = rng;
-        if (part) rng.state = add128(mul128(rng.state, s.jump_mult[1]), mul128(rng.inc, s.jump_add[1]));
-        r2.state = add128(mul128(r2.state, part ? s.jump_mult[2] : s.jump_mult[0]),
-                          mul128(r2.inc, part ? s.jump_add[2] : s.jump_add[0]));
-        const int i0 = 2 * part * Lseg;
-        float* row = x0s + al * S;
-#pragma unroll 2
-        for (int i = 0; i < Lseg; ++i) {
-            const int ia = i0 + i, ib = i0 + Lseg + i;
-            const double ua = rng.uniform(s.x0_lo, s.x0_range);
-            const double ub = r2.uniform(s.x0_lo, s.x0_range);
-            if (ia < S) row[ia] = SC ? (float)(s.sdt * ua) : (float)ua;
-            if (ib < S) row[ib] = SC ? (float)(s.sdt * ub) : (float)ub;
-        }
-        } else {
+        // lane part 1 jumps ahead over the first half of the stream
         constexpr int S0 = (S + 1) / 2;
         if (part) rng.state = add128(mul128(rng.state, s.jump_mult[3]), mul128(rng.inc, s.jump_add[3]));
         const int i0 = part ? S0 : 0, i1 = part ? S : S0;
         for (int i = i0; i < i1; ++i)
             x0s[al * S + i] = SC ? (float)(s.sdt * rng.uniform(s.x0_lo, s.x0_range))
                                  : (float)rng.uniform(s.x0_lo, s.x0_range);
-        }
     }
-    }
-    if constexpr (L::kSmemG) mbar_wait(bar, 0);
 
     // ---- per-problem scale 2^sc for -K*G ------------------------------------
     const double K = s.dt * eps_p[prob];
     double gmax = 0.0;
-#if IL_GMAX_WIDE
-    // all N^2/32 loads of this lane in flight at once (the first touch of G
-    // comes from HBM), folded into 4 independent partial max / sum chains
-    {
-        constexpr int kPer = N * N / 32, kAcc = kPer >= 4 ? 4 : kPer;
-        double v[kPer];
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) v[k] = fabs(L::kSmemG ? G[lane + 32 * k] : __ldg(G + lane + 32 * k));
-        double gm[kAcc], sm[kAcc];
-#pragma unroll
-        for (int a = 0; a < kAcc; ++a) gm[a] = sm[a] = 0.0;
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            gm[k % kAcc] = fmax(gm[k % kAcc], v[k]);
-            sm[k % kAcc] += v[k];
-        }
-#pragma unroll
-        for (int a = 0; a < kAcc; ++a) gmax = fmax(gmax, gm[a]);
-        if (screened) {
-            double mag = 0.0;  // sum |G| + sum |b|: the screen bound, parked in shared memory
-#pragma unroll
-            for (int a = 0; a < kAcc; ++a) mag += sm[a];
-            for (int i = lane; i < N; i += 32) mag += fabs(bv_p[i]);
-            mag = warp_sum(mag);
-            if (lane == 0) reinterpret_cast<double*>(frag + L::kKgF4 - 1)[0] = mag;
-        }
-    }
-#else
     if (screened) {
         double mag = 0.0;  // sum |G| + sum |b|: the screen bound, parked in shared memory
 #pragma unroll 4
         for (int i = lane; i < N * N; i += 32) {
-            const double v = fabs(L::kSmemG ? G[i] : __ldg(G + i));
+            const double v = fabs(__ldg(G + i));
             gmax = fmax(gmax, v);
             mag += v;
         }
@@ -290,9 +153,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         if (lane == 0) reinterpret_cast<double*>(frag + L::kKgF4 - 1)[0] = mag;
     } else {
 #pragma unroll 4
-        for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(L::kSmemG ? G[i] : __ldg(G + i)));
+        for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(__ldg(G + i)));
     }
-#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
     int ex = 0;
@@ -336,7 +198,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int r = 16 * kt + 2 * t + (q & 1) + 8 * (q >> 1);
-                f[q] = r < N ? (float)(-Ks * (L::kSmemG ? G[r * N + c] : __ldg(G + r * N + c))) : 0.f;
+                f[q] = r < N ? (float)(-Ks * __ldg(G + r * N + c)) : 0.f;
             }
             uint32_t h01, l01, h23, l23;
             split_h2(make_float2(f[0], f[1]), h01, l01);
@@ -344,36 +206,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             frag[(kt * NT + n) * 32 + lane] = make_uint4(h01, h23, l01, l23);
         }
     }
-    if constexpr (CPLX) {
-        // G = [[R, -I], [I, R]] (n = N/2 = 16 KT/2 real spins first): the
-        // Karatsuba refresh needs B = -Ks (R - I) beside -Ks R (k-tiles of the
-        // real rows) and -Ks I (k-tiles of the imaginary rows), in the slots of
-        // the (real rows x imaginary columns) tiles it does not read
-        constexpr int KH = KT / 2, NH = NT / 2;
-#pragma unroll
-        for (int kt = 0; kt < KH; ++kt) {
-#pragma unroll
-            for (int n = 0; n < NH; ++n) {
-                const int c = 8 * n + g;
-                float f[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int r = 16 * kt + 2 * t + (q & 1) + 8 * (q >> 1);
-                    const double gr = L::kSmemG ? G[r * N + c] : __ldg(G + r * N + c);
-                    const double gi = L::kSmemG ? G[(r + N / 2) * N + c] : __ldg(G + (r + N / 2) * N + c);
-                    f[q] = (float)(-Ks * (gr - gi));
-                }
-                uint32_t h01, l01, h23, l23;
-                split_h2(make_float2(f[0], f[1]), h01, l01);
-                split_h2(make_float2(f[2], f[3]), h23, l23);
-                frag[(kt * NT + n + NH) * 32 + lane] = make_uint4(h01, h23, l01, l23);
-            }
-        }
-    }
-    // per-thread spin constants: Ks g_i and -Ks b_i for spins 8n+2t+{0,1}
-#if IL_KG_SMEM
-    // kept in shared memory and re-read at every refresh: the registers go to
-    // the Euler update's scheduling instead
+    // per-thread spin constants Ks g_i and -Ks b_i for spins 8n+2t+{0,1}: kept
+    // in shared memory and re-read at every refresh (the registers go to the
+    // Euler update's scheduling instead)
     float4* kgs = reinterpret_cast<float4*>(frag + L::kKgF4);
 #pragma unroll
     for (int n = 0; n < NT; ++n) {
@@ -381,95 +216,19 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         kgs[n * 32 + lane] = make_float4((float)(Ks * gv_p[i]), (float)(Ks * gv_p[i + 1]),
                                          (float)(-Ks * bv_p[i]), (float)(-Ks * bv_p[i + 1]));
     }
-    auto kg_ld = [&](int n) {
+    auto kg4 = [&](int n) {
         float4 r;
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                      : "r"(smem_u32(kgs + n * 32 + lane)));
         return r;
     };
-    auto kg4 = [&](int n) { return kg_ld(n); };
-#define IL_KG(n) ([&] { const float4 r_ = kg_ld(n); return make_float2(r_.x, r_.y); }())
-#define IL_NKB(n) ([&] { const float4 r_ = kg_ld(n); return make_float2(r_.z, r_.w); }())
-#else
-    float2 Kg[NT], nKb[NT];
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-        const int i = 8 * n + 2 * t;
-        Kg[n] = make_float2((float)(Ks * gv_p[i]), (float)(Ks * gv_p[i + 1]));
-        nKb[n] = make_float2((float)(-Ks * bv_p[i]), (float)(-Ks * bv_p[i + 1]));
-    }
-    auto kg4 = [&](int n) { return make_float4(Kg[n].x, Kg[n].y, nKb[n].x, nKb[n].y); };
-#define IL_KG(n) Kg[n]
-#define IL_NKB(n) nKb[n]
-#endif
+    auto nkb = [&](int n) {
+        const float4 r = kg4(n);
+        return make_float2(r.z, r.w);
+    };
     __syncwarp();
 
-    // Coupling product for complex-structured G (CPLX): with n = N/2 real
-    // spins first, G = [[R, -I], [I, R]] and B = -Ks G,
-    //   D_re = X + Y, D_im = Z - X + Y,  X = W_re (-Ks R), Y = W_im (-Ks I),
-    //   Z = (W_re + W_im)(-Ks (R - I)),
-    // 3 products of K = N/2 (18 HMMA at N = 32) instead of 4 (24 HMMA).
-    [[maybe_unused]] auto cplx_product = [&](const float2 (&w)[2][NT], float (&acc)[NT][4]) {
-                // D_re = X + Y, D_im = Z - X + Y with X = V_re (-Ks R), Y = V_im (-Ks I),
-                // Z = (V_re + V_im)(-Ks (R - I)): 3 products of K = N/2 instead of 4
-                constexpr int KH = KT / 2, NH = NT / 2;
-                auto afrag = [&](int kt, int off, uint32_t (&ahi)[4], uint32_t (&alo)[4]) {
-                    // k-tile kt of the half starting at n-tile off; off < 0: the sum
-                    if (off >= 0) {
-                        split_h2(w[0][off + 2 * kt], ahi[0], alo[0]);
-                        split_h2(w[1][off + 2 * kt], ahi[1], alo[1]);
-                        split_h2(w[0][off + 2 * kt + 1], ahi[2], alo[2]);
-                        split_h2(w[1][off + 2 * kt + 1], ahi[3], alo[3]);
-                    } else {
-                        split_h2(__fadd2_rn(w[0][2 * kt], w[0][NH + 2 * kt]), ahi[0], alo[0]);
-                        split_h2(__fadd2_rn(w[1][2 * kt], w[1][NH + 2 * kt]), ahi[1], alo[1]);
-                        split_h2(__fadd2_rn(w[0][2 * kt + 1], w[0][NH + 2 * kt + 1]), ahi[2], alo[2]);
-                        split_h2(__fadd2_rn(w[1][2 * kt + 1], w[1][NH + 2 * kt + 1]), ahi[3], alo[3]);
-                    }
-                };
-                auto mma3 = [&](float (&d)[4], const uint32_t (&ahi)[4], const uint32_t (&alo)[4],
-                                const uint4 f) {
-                    if (SPLIT) {
-                        mma_f16(d, alo, f.x, f.y);
-                        mma_f16(d, ahi, f.z, f.w);
-                    }
-                    mma_f16(d, ahi, f.x, f.y);
-                };
-                // Y into the real-half accumulators
-#pragma unroll
-                for (int kt = 0; kt < KH; ++kt) {
-                    uint32_t ahi[4], alo[4];
-                    afrag(kt, NH, ahi, alo);
-#pragma unroll
-                    for (int n = 0; n < NH; ++n) mma3(acc[n], ahi, alo, frag[((kt + KH) * NT + n) * 32 + lane]);
-                }
-                // copy Y to the imaginary half, then X on top of Y (real half)
-#pragma unroll
-                for (int n = 0; n < NH; ++n)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[n + NH][q] = acc[n][q];
-#pragma unroll
-                for (int kt = 0; kt < KH; ++kt) {
-                    uint32_t ahi[4], alo[4];
-                    afrag(kt, 0, ahi, alo);
-#pragma unroll
-                    for (int n = 0; n < NH; ++n) mma3(acc[n], ahi, alo, frag[(kt * NT + n) * 32 + lane]);
-                }
-                // imaginary half: Y - X = 2 Y - (X + Y), then + Z
-#pragma unroll
-                for (int n = 0; n < NH; ++n)
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) acc[n + NH][q] = fmaf(2.f, acc[n + NH][q], -acc[n][q]);
-#pragma unroll
-                for (int kt = 0; kt < KH; ++kt) {
-                    uint32_t ahi[4], alo[4];
-                    afrag(kt, -1, ahi, alo);
-#pragma unroll
-                    for (int n = 0; n < NH; ++n)
-                        mma3(acc[n + NH], ahi, alo, frag[(kt * NT + n + NH) * 32 + lane]);
-                }
-    };
     int until_refresh = 0;
 #pragma unroll kStepUnroll
     for (int step = 0; step < s.n_steps; ++step) {
@@ -478,7 +237,6 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             // ---- refresh: v = x1 + x2, M' = -Ks G v on tensor cores -----------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
-#if IL_PB2
             // packed partial sums of -Ks b.v over the thread's spin pairs; every
             // lane of a quad sums the same pairs in the same order, so the two
             // owner lanes of an aux spin still agree bit for bit
@@ -488,20 +246,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
                     v[h][n] = __fadd2_rn(xA[h][n], xB[h][n]);
-                    p2 = __ffma2_rn(IL_NKB(n), v[h][n], p2);
+                    p2 = __ffma2_rn(nkb(n), v[h][n], p2);
                 }
                 pb[h] = p2.x + p2.y;
             }
-#else
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int n = 0; n < NT; ++n) {
-                    v[h][n] = __fadd2_rn(xA[h][n], xB[h][n]);
-                    pb[h] = fmaf(IL_NKB(n).x, v[h][n].x, pb[h]);
-                    pb[h] = fmaf(IL_NKB(n).y, v[h][n].y, pb[h]);
-                }
-#endif
             // aux states of both anneals of the quad, from their owner lanes
             const float xa0 = __shfl_sync(0xffffffffu, xa, (lane & ~3) | 0);
             const float xa1 = __shfl_sync(0xffffffffu, xa, (lane & ~3) | 1);
@@ -518,43 +266,6 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             float acc[NT][4];
 #pragma unroll
             for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-#if IL_SPLIT_ACC
-            float acc2[NT][4];
-#pragma unroll
-            for (int n = 0; n < NT; ++n) acc2[n][0] = acc2[n][1] = acc2[n][2] = acc2[n][3] = 0.f;
-#endif
-#if IL_NOUTER
-            // all A fragments first, then one n-tile at a time: acc[n] completes
-            // early, so its coupling assembly (and the Euler step, in the same
-            // block) can overlap the tensor work of the next tiles
-            uint32_t AH[KT][4], AL[KT][4];
-#pragma unroll
-            for (int kt = 0; kt < KT; ++kt) {
-                split_h2(v[0][2 * kt], AH[kt][0], AL[kt][0]);
-                split_h2(v[1][2 * kt], AH[kt][1], AL[kt][1]);
-                if (2 * kt + 1 < NT) {
-                    split_h2(v[0][2 * kt + 1], AH[kt][2], AL[kt][2]);
-                    split_h2(v[1][2 * kt + 1], AH[kt][3], AL[kt][3]);
-                } else {
-                    AH[kt][2] = AH[kt][3] = AL[kt][2] = AL[kt][3] = 0u;
-                }
-            }
-#pragma unroll
-            for (int n = 0; n < NT; ++n) {
-#pragma unroll
-                for (int kt = 0; kt < KT; ++kt) {
-                    const uint4 f = frag[(kt * NT + n) * 32 + lane];
-                    if (SPLIT) {
-                        mma_f16(acc[n], AL[kt], f.x, f.y);
-                        mma_f16(acc[n], AH[kt], f.z, f.w);
-                    }
-                    mma_f16(acc[n], AH[kt], f.x, f.y);
-                }
-            }
-#else
-            if constexpr (CPLX) {
-                cplx_product(v, acc);
-            } else {
 #pragma unroll
             for (int kt = 0; kt < KT; ++kt) {
                 // A fragment: a0 = (g, 2t..), a1 = (g+8, 2t..), a2 = (g, 2t+8..), a3 = (g+8, 2t+8..)
@@ -571,119 +282,26 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 for (int n = 0; n < NT; ++n) {
                     const uint4 f = frag[(kt * NT + n) * 32 + lane];
                     if (SPLIT) {
-#if IL_SPLIT_ACC
-                        mma_f16(acc2[n], alo, f.x, f.y);
-                        mma_f16(acc2[n], ahi, f.z, f.w);
-#else
                         mma_f16(acc[n], alo, f.x, f.y);
                         mma_f16(acc[n], ahi, f.z, f.w);
-#endif
                     }
                     mma_f16(acc[n], ahi, f.x, f.y);
                 }
             }
-            }
-#endif
-#if IL_FUSE_Q
-            // C-independent part of this step's Euler update (x^2, the
-            // divergence max, the x- and e-factors) in the refresh's basic
-            // block, where it can fill the tensor-core latency; the remaining
-            // operations follow the assembly below.  Same operations, same
-            // order as euler_pair: bit-identical.
-            float2 qA[2][NT], qB[2][NT];
-            [[maybe_unused]] float2 rA[2][NT], rB[2][NT];
-#pragma unroll
-            for (int h = 0; h < 2; ++h)
-#pragma unroll
-                for (int n = 0; n < NT; ++n) {
-                    const float2 a2 = __fmul2_rn(xA[h][n], xA[h][n]);
-                    dv[h][n & 1] = max_nan3(dv[h][n & 1], a2.x, a2.y);
-                    qA[h][n] = __ffma2_rn(make_float2(s.ndt, s.ndt), a2, make_float2(s.alpha, s.alpha));
-                    const float2 b2 = __fmul2_rn(xB[h][n], xB[h][n]);
-                    dv[h][n & 1] = max_nan3(dv[h][n & 1], b2.x, b2.y);
-                    qB[h][n] = __ffma2_rn(make_float2(s.ndt, s.ndt), b2, make_float2(s.alpha, s.alpha));
-                    if constexpr (!SAME_QR) {
-                        rA[h][n] = __ffma2_rn(make_float2(s.ndtz, s.ndtz), a2, make_float2(s.beta, s.beta));
-                        rB[h][n] = __ffma2_rn(make_float2(s.ndtz, s.ndtz), b2, make_float2(s.beta, s.beta));
-                    }
-                }
-#endif
             // ---- coupling assembly: C_s = M' + Ks g x_self - Ks b xa ----------
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const float xah = h ? xa1 : xa0;
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
-#if IL_SPLIT_ACC
-                    const float2 m2 = SPLIT ? __fadd2_rn(make_float2(acc2[n][2 * h], acc2[n][2 * h + 1]),
-                                                         make_float2(acc[n][2 * h], acc[n][2 * h + 1]))
-                                            : make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
-#else
                     const float2 m2 = make_float2(acc[n][2 * h], acc[n][2 * h + 1]);
-#endif
                     const float4 kk = kg4(n);
                     const float2 u2 = __ffma2_rn(make_float2(kk.z, kk.w), make_float2(xah, xah), m2);
                     CA[h][n] = __ffma2_rn(make_float2(kk.x, kk.y), xA[h][n], u2);
                     CB[h][n] = __ffma2_rn(make_float2(kk.x, kk.y), xB[h][n], u2);
-#if IL_FUSE_Q
-                    xA[h][n] = __ffma2_rn(eA[h][n], CA[h][n], __fmul2_rn(xA[h][n], qA[h][n]));
-                    xB[h][n] = __ffma2_rn(eB[h][n], CB[h][n], __fmul2_rn(xB[h][n], qB[h][n]));
-                    if constexpr (SAME_QR) {
-                        eA[h][n] = __fmul2_rn(eA[h][n], qA[h][n]);
-                        eB[h][n] = __fmul2_rn(eB[h][n], qB[h][n]);
-                    } else {
-                        eA[h][n] = __fmul2_rn(eA[h][n], rA[h][n]);
-                        eB[h][n] = __fmul2_rn(eB[h][n], rB[h][n]);
-                    }
-#if !IL_BOUND_FLOOR
-                    eA[h][n] = floor2(eA[h][n], e_floor);
-                    eB[h][n] = floor2(eB[h][n], e_floor);
-#endif
-#endif
                 }
             }
         }
-#if IL_FUSE_Q
-        else
-#endif
-        {
-#if IL_EULER_GROUP
-        // the same per-pair operations as euler_pair, issued stage by stage
-        // over groups of 4 spin pairs so that dependent instructions are 4
-        // apart (the max.NaN of the divergence test is order-independent)
-        static_assert(IL_BOUND_FLOOR, "grouped Euler step assumes the floor bound");
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-#pragma unroll
-            for (int n0 = 0; n0 < NT; n0 += 2) {
-                float2* xs[4] = {&xA[h][n0], &xB[h][n0], &xA[h][n0 + 1 < NT ? n0 + 1 : n0],
-                                 &xB[h][n0 + 1 < NT ? n0 + 1 : n0]};
-                float2* es[4] = {&eA[h][n0], &eB[h][n0], &eA[h][n0 + 1 < NT ? n0 + 1 : n0],
-                                 &eB[h][n0 + 1 < NT ? n0 + 1 : n0]};
-                const float2* cs[4] = {&CA[h][n0], &CB[h][n0], &CA[h][n0 + 1 < NT ? n0 + 1 : n0],
-                                       &CB[h][n0 + 1 < NT ? n0 + 1 : n0]};
-                const int ng = n0 + 1 < NT ? 4 : 2;
-                float2 x2[4], q[4], r[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (i < ng) x2[i] = __fmul2_rn(*xs[i], *xs[i]);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (i < ng) {
-                        dv[h][(n0 + (i >> 1)) & 1] = max_nan3(dv[h][(n0 + (i >> 1)) & 1], x2[i].x, x2[i].y);
-                        q[i] = __ffma2_rn(make_float2(s.ndt, s.ndt), x2[i], make_float2(s.alpha, s.alpha));
-                        r[i] = SAME_QR ? q[i]
-                                       : __ffma2_rn(make_float2(s.ndtz, s.ndtz), x2[i], make_float2(s.beta, s.beta));
-                    }
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (i < ng) *xs[i] = __ffma2_rn(*es[i], *cs[i], __fmul2_rn(*xs[i], q[i]));
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (i < ng) *es[i] = __fmul2_rn(*es[i], r[i]);
-            }
-        }
-#else
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
 #pragma unroll
@@ -696,8 +314,6 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                     euler_pair<SAME_QR>(xB[h][n], eB[h][n], CB[h][n], s, e_floor, dv[h][n & 1]);
                 }
             }
-        }
-#endif
         }
 #if IL_BOUND_FLOOR
         // e' = max(e_floor, e r).  Every e of this thread stays >= e_lb, a
@@ -796,12 +412,6 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         dflag[h] = SC ? !(d >= s.qthr) : !(d <= s.thr2);
         if (t == 0) diverged[row] = dflag[h] ? 1 : 0;
     }
-#if IL_PROBE_NO_ENERGY
-    if (screened) {
-        if (t < 2) energies[row0 + g + 8 * t] = (double)(pos[t] ^ neg[t]);
-        return;
-    }
-#endif
     if (screened) {
         // Selection screen: E + 2 tr G in FP32 from the tensor cores.  u =
         // s_A + s_B in {-2, 0, 2} is exact in f16, so two passes over the
@@ -814,37 +424,21 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             for (int n = 0; n < NT; ++n)
                 u[h][n] = make_float2((xA[h][n].x >= 0.f ? 1.f : -1.f) + (xB[h][n].x >= 0.f ? 1.f : -1.f),
                                       (xA[h][n].y >= 0.f ? 1.f : -1.f) + (xB[h][n].y >= 0.f ? 1.f : -1.f));
-        // N = 32: lane i's column of G (and G[i][i], b[i]) for the FP64
-        // re-evaluation, loaded now so the L2 round trip overlaps the screen
-        constexpr bool kPre = (N == 32) && IL_SCREEN_PREFETCH;
-        [[maybe_unused]] double gcol[kPre ? 32 : 1], gdiag = 0.0, bown = 0.0;
-        if constexpr (kPre) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) gcol[j] = L::kSmemG ? G[j * N + lane] : __ldg(G + j * N + lane);
-            gdiag = L::kSmemG ? G[lane * N + lane] : __ldg(G + lane * N + lane);
-            bown = bv_p[lane];
-        }
         float acc[NT][4];
 #pragma unroll
         for (int n = 0; n < NT; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
-        // (CPLX: the staged tiles are the 3-product ones; u is exact in f16, so
-        // its lo part is zero and the product has the same error bound)
-        if constexpr (CPLX) {
-            cplx_product(u, acc);
-        } else {
 #pragma unroll
-            for (int kt = 0; kt < KT; ++kt) {
-                uint32_t a[4];
-                a[0] = h2_bits(__float22half2_rn(u[0][2 * kt]));
-                a[1] = h2_bits(__float22half2_rn(u[1][2 * kt]));
-                a[2] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[0][2 * kt + 1])) : 0u;
-                a[3] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[1][2 * kt + 1])) : 0u;
+        for (int kt = 0; kt < KT; ++kt) {
+            uint32_t a[4];
+            a[0] = h2_bits(__float22half2_rn(u[0][2 * kt]));
+            a[1] = h2_bits(__float22half2_rn(u[1][2 * kt]));
+            a[2] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[0][2 * kt + 1])) : 0u;
+            a[3] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(u[1][2 * kt + 1])) : 0u;
 #pragma unroll
-                for (int n = 0; n < NT; ++n) {
-                    const uint4 f = frag[(kt * NT + n) * 32 + lane];
-                    mma_f16(acc[n], a, f.z, f.w);
-                    mma_f16(acc[n], a, f.x, f.y);
-                }
+            for (int n = 0; n < NT; ++n) {
+                const uint4 f = frag[(kt * NT + n) * 32 + lane];
+                mma_f16(acc[n], a, f.z, f.w);
+                mma_f16(acc[n], a, f.x, f.y);
             }
         }
         // unscaled FP32-screen energies (without -2 tr G) of rows g, g+8
@@ -856,8 +450,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             for (int n = 0; n < NT; ++n) {
                 q = fmaf(u[h][n].x, acc[n][2 * h], q);
                 q = fmaf(u[h][n].y, acc[n][2 * h + 1], q);
-                l = fmaf(IL_NKB(n).x, u[h][n].x, l);
-                l = fmaf(IL_NKB(n).y, u[h][n].y, l);
+                l = fmaf(nkb(n).x, u[h][n].x, l);
+                l = fmaf(nkb(n).y, u[h][n].y, l);
             }
             float e = fmaf(xa_h[h] >= 0.f ? 2.f : -2.f, l, q);  // -Ks (u'Gu + 2 s_aux b'u)
             e += __shfl_xor_sync(0xffffffffu, e, 1);
@@ -883,19 +477,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         double* w = reinterpret_cast<double*>(frag);  // fragments are consumed
         __syncwarp();
         double tr = 0.0;
-        if constexpr (kPre) {
-            tr = gdiag;
-        } else {
-            for (int i = lane; i < N; i += 32) tr += G[(int64_t)i * N + i];
-        }
+        for (int i = lane; i < N; i += 32) tr += G[(int64_t)i * N + i];
         tr = warp_sum(tr);
-#if IL_PROBE_CAND
-        int n_eval = 0, n_cand0 = __popc(cand);
-#endif
         while (cand) {
-#if IL_PROBE_CAND
-            ++n_eval;
-#endif
             const int l = __ffs(cand) - 1;
             const uint64_t cp = __shfl_sync(0xffffffffu, my_pos, l);
             const uint64_t cn = __shfl_sync(0xffffffffu, my_neg, l);
@@ -906,26 +490,15 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 w[j] = (double)((int)((cp >> j) & 1u) - (int)((cn >> j) & 1u));
             __syncwarp();
             double q = 0.0, li = 0.0;
-            if constexpr (kPre) {  // same operations and order as the loop below
-                double gu[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-#pragma unroll
-                    for (int r = 0; r < 4; ++r) gu[r] = fma(gcol[j + r], w[j + r], gu[r]);
-                q = fma(w[lane], (gu[0] + gu[1]) + (gu[2] + gu[3]), q);
-                li = fma(bown, w[lane], li);
-            } else {
             for (int i = lane; i < N; i += 32) {
                 double gu[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int j = 0; j < N; j += 4)
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
-                        gu[r] = fma(L::kSmemG ? G[(j + r) * N + i] : __ldg(G + (int64_t)(j + r) * N + i),
-                                    w[j + r], gu[r]);
+                        gu[r] = fma(__ldg(G + (int64_t)(j + r) * N + i), w[j + r], gu[r]);
                 q = fma(w[i], (gu[0] + gu[1]) + (gu[2] + gu[3]), q);
                 li = fma(bv_p[i], w[i], li);
-            }
             }
             __syncwarp();
             q = warp_sum(q);
@@ -937,20 +510,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             cand &= ~__ballot_sync(0xffffffffu, same);
         }
         if (t < 2) energies[row0 + g + 8 * t] = my_e;
-#if IL_PROBE_CAND
-        if (lane == 0 && (blockIdx.x % 512) == 0)
-            printf("cand %d eval %d\n", n_cand0, n_eval);
-#endif
         return;
     }
     // FP64 energies.  Row sums use G's symmetry: sum_j s_j G[j][i] reads row j
     // at this lane's columns i = 8n+2t+{0,1} (16-byte loads), with s_j decoded
     // once per j for both anneals.
     const double* bg = bv_p;
-#if IL_PROBE_NO_ENERGY
-    if (t < 2) energies[row0 + g + 8 * t] = (double)(pos[t] ^ neg[t]);
-    return;
-#endif
     double rs[2][2 * NT];
 #pragma unroll
     for (int k = 0; k < 2 * NT; ++k) rs[0][k] = rs[1][k] = 0.0;
@@ -960,8 +525,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         const double* Gj = G + (int64_t)j * N + 2 * t;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-            const double2 gv = L::kSmemG ? *reinterpret_cast<const double2*>(Gj + 8 * n)
-                                         : __ldg(reinterpret_cast<const double2*>(Gj + 8 * n));
+            const double2 gv = __ldg(reinterpret_cast<const double2*>(Gj + 8 * n));
             rs[0][2 * n] = fma(gv.x, s0, rs[0][2 * n]);
             rs[0][2 * n + 1] = fma(gv.y, s0, rs[0][2 * n + 1]);
             rs[1][2 * n] = fma(gv.x, s1, rs[1][2 * n]);
@@ -999,26 +563,19 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     }
 }
 
-template <int NT, bool SPLIT, bool SAME_QR, bool CPLX = false>
+template <int NT, bool SPLIT, bool SAME_QR>
 int launch_cfg(const double* G, const double* g, const double* b, const uint64_t* base_seed,
                const double* eps_p, int64_t n_tasks, int tiles, const FastScalars& fs,
                int8_t* spins, uint8_t* diverged, double* energies, bool screened,
                cudaStream_t st) {
     const int64_t blocks = (n_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
     IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
-    // distinct problems per CTA (periodic in the block index, period <= tiles)
-    FastScalars f2 = fs;
-    f2.n_slots = 1;
-    for (int64_t blk = 0; blk < std::min<int64_t>(blocks, tiles); ++blk) {
-        const int64_t t0 = blk * kWarpsPerCta, t1 = std::min(n_tasks, t0 + kWarpsPerCta) - 1;
-        f2.n_slots = std::max<int>(f2.n_slots, (int)(t1 / tiles - t0 / tiles + 1));
-    }
-    const size_t smem = FastLayout<NT>::smem(f2.n_slots);
-    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR, CPLX>;
+    const size_t smem = FastLayout<NT>::kWarpBytes;
+    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR>;
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     IL_LAUNCH(kProfAnneal, st, fn<<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(G, g, b, base_seed, eps_p, n_tasks, tiles,
-                                                        f2, spins, diverged, energies, screened););
+                                                        fs, spins, diverged, energies, screened););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
@@ -1027,19 +584,9 @@ template <int NT>
 int launch_nt(const double* G, const double* g, const double* b, const uint64_t* base_seed,
               const double* eps_p, int64_t P, int B, const FastScalars& fs, bool split,
               bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, bool screened,
-              bool cplx, cudaStream_t st) {
+              cudaStream_t st) {
     const int tiles = B / 16;
     const int64_t n_tasks = P * tiles;
-    // complex-structured G (every Ising built from a complex Gram): the
-    // 3-product refresh, for n = N/2 a multiple of 16 (real / imaginary spins
-    // on whole k-tiles) at the default operating point
-    if constexpr ((NT == 4 || NT == 8) && IL_CPLX_MVM) {
-        if (cplx && same_qr)
-            return split ? launch_cfg<NT, true, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                            spins, diverged, energies, screened, st)
-                         : launch_cfg<NT, false, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles,
-                                                             fs, spins, diverged, energies, screened, st);
-    }
     if (split) {
         return same_qr ? launch_cfg<NT, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
                                                    spins, diverged, energies, screened, st)
@@ -1082,7 +629,7 @@ bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st, int screen_rows, bool cplx) {
+                       double* energies, cudaStream_t st, int screen_rows) {
     if (!fast_anneal_supported(N, B, s)) {
         set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
         return IL_ERR_UNSUPPORTED;
@@ -1125,7 +672,7 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
         return launch_anneal_umma(G, g, b, base_seed, eps_p, P, N, B, &fs, split, same_qr, spins,
                                   diverged, energies, screened, st);
 #define IL_NT(k) \
-    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, cplx, st)
+    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, st)
     switch (N / 8) {
         IL_NT(1);
         IL_NT(2);

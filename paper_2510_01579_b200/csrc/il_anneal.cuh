@@ -31,7 +31,6 @@ struct FastScalars {
     double x0_lo, x0_range;
     U128 jump_mult[4], jump_add[4];  // PCG64 advance by 1, 2, 3 quarter segments; [3]: half
     int f_mvm, n_steps;
-    int n_slots;  // problems whose G a CTA stages (IL_TMA_G)
     double sdt;   // sqrt(dt): scale of the stored state (IL_SCALED_X)
     float qthr;   // alpha - dt thr^2: q below it means |x| > thr (IL_SCALED_X)
     int b_valid;  // anneal rows per problem that enter the selection (screened energies)

@@ -26,17 +26,14 @@ int launch_anneal_exact(const double* G, const double* g, const double* b, const
 // the shape is not instantiated.
 // Energies: the FP64 energy of every anneal; or, with screen_rows > 0, only of
 // the anneals among the first screen_rows rows of each problem that can be the
-// FP64 argmin of those rows (+inf for the others).  cplx_structured: G is
-// c^2 [[Re A, -Im A], [Im A, Re A]] (A Hermitian) -- every Ising the library
-// builds from a complex Gram -- enabling the 3-product refresh:
-// an FP32 tensor-core screen bounds every energy to within 2^-13 (sum|G| +
-// sum|b|) and only the distinct configurations within twice that of the
-// minimum are evaluated in FP64.  The argmin (ties -> lowest row) is the same.
+// FP64 argmin of those rows (+inf for the others): an FP32 tensor-core
+// screen bounds every energy to within 2^-13 (sum|G| + sum|b|) and only the
+// distinct configurations within twice that of the minimum are evaluated in
+// FP64.  The argmin (ties -> lowest row) is the same.
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st, int screen_rows = 0,
-                       bool cplx_structured = false);
+                       double* energies, cudaStream_t st, int screen_rows = 0);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
 // The same anneal with the coupling product on tcgen05 (anneal_umma.cu);
 // launch_anneal_fast dispatches to it when enabled and supported.

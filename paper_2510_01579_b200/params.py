@@ -4,9 +4,11 @@ the B200 arithmetic mode.
 ``precision`` selects the anneal arithmetic:
   * ``"fp64_exact"`` — FP64 in the reference kernel's evaluation order, no
     FMA contraction: bit-identical to the reference "ext" backend;
-  * ``"fp32"`` (default) — FP32 state, coupling product on tensor cores with a
-    3xTF32 split (FP32-accurate); the throughput mode;
-  * ``"tf32"`` — single-pass TF32 coupling product (fastest, least accurate).
+  * ``"fp32"`` (default) — FP32 state, coupling product on tensor cores as a
+    3-pass f16 hi/lo split (hi*hi + lo*hi + hi*lo, FP32 accumulate;
+    FP32-accurate); the throughput mode;
+  * ``"tf32"`` — single-pass f16 coupling product (11-bit significand, like
+    TF32; fastest, least accurate).
 
 Reference ``CacParams`` objects (no ``precision`` attribute) are accepted
 everywhere and run in ``DEFAULT_PRECISION``.
