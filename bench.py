@@ -169,10 +169,18 @@ def cpu_kind() -> str:
 
 
 def host_cores() -> int:
+    """Physical cores available to this process (BASELINE.md section 3:
+    psutil.cpu_count(logical=False)), capped by the CPU affinity mask."""
     try:
-        return len(os.sched_getaffinity(0))
+        avail = len(os.sched_getaffinity(0))
     except AttributeError:
-        return os.cpu_count() or 1
+        avail = os.cpu_count() or 1
+    try:
+        import psutil
+        phys = psutil.cpu_count(logical=False) or avail
+    except ImportError:
+        phys = avail
+    return max(1, min(avail, phys))
 
 
 # ---------------------------------------------------------------------------
@@ -185,7 +193,9 @@ def run_reference(args) -> None:
     import multiprocessing as mp
     cores = host_cores()
     kind = cpu_kind()
-    per_step = max(cores * 4, 64)
+    # ~128 REs per process per step (about 2 s of CPU work per step at the
+    # measured ~8 k det/s on 16 cores): pool dispatch overhead stays small
+    per_step = cores * 128
     pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init)
     pool.map(_cpu_worker, cpu_instances(cores), chunksize=1)
     for _ in range(args.warmup):
@@ -225,6 +235,41 @@ def anneal_traffic():
         return int(d["dram_bytes_read"]) + int(d["dram_bytes_write"])
     except (OSError, KeyError, ValueError):
         return None
+
+
+def headline_slot(dev, lo=0, hi=None):
+    """The headline workload (BASELINE.json configs[2]): one 273-PRB slot of
+    16x16 16-QAM uplink REs at 20 dB, i.i.d. Rayleigh, generated on the device
+    from MASTER_SEED identically on every rank and sliced to [lo, hi); the
+    detector seed of RE t is derive_seed(MASTER_SEED, 1, 0, t, 3) (the
+    reference sweep's key, sweeps.py:130).  Returns H, y, noise_var, seeds,
+    truth (level indices) of the slice."""
+    import torch
+
+    from paper_2510_01579_b200 import batched
+    P_all = N_PRB * 12 * 14
+    hi = P_all if hi is None else hi
+    gen = torch.Generator(device=dev).manual_seed(MASTER_SEED)
+    H = torch.complex(torch.randn(P_all, N_R, N_T, dtype=torch.float64, device=dev, generator=gen),
+                      torch.randn(P_all, N_R, N_T, dtype=torch.float64, device=dev, generator=gen))
+    H *= math.sqrt(0.5)
+    m = int(math.isqrt(ORDER))
+    levels = (torch.arange(-(m - 1), m, 2, dtype=torch.float64, device=dev)
+              / math.sqrt(2 * (m * m - 1) / 3))
+    sym_re = torch.randint(0, m, (P_all, N_T), device=dev, generator=gen)
+    sym_im = torch.randint(0, m, (P_all, N_T), device=dev, generator=gen)
+    x = torch.complex(levels[sym_re], levels[sym_im])
+    s2 = N_T / 10 ** (SNR_DB / 10)
+    noise = torch.complex(torch.randn(P_all, N_R, dtype=torch.float64, device=dev, generator=gen),
+                          torch.randn(P_all, N_R, dtype=torch.float64, device=dev, generator=gen))
+    y = torch.einsum("prt,pt->pr", H, x) + noise * math.sqrt(s2 / 2)
+    nv = torch.full((P_all,), s2, dtype=torch.float64, device=dev)
+    parts = np.stack([np.full(P_all, MASTER_SEED), np.full(P_all, 1), np.zeros(P_all),
+                      np.arange(P_all), np.full(P_all, 3)], axis=1).astype(np.uint64)
+    seeds = batched.derive_seeds(parts)  # detector seed of RE t: derive_seed(seed, 1, 0, t, 3)
+    truth = torch.stack([sym_re[lo:hi], sym_im[lo:hi]], -1).to(torch.uint8)
+    return (H[lo:hi].contiguous(), y[lo:hi].contiguous(), nv[lo:hi].contiguous(),
+            seeds[lo:hi].contiguous(), truth)
 
 
 def _synthetic_uplink(dev, P, n_t, order, snr_db, seed):
@@ -271,6 +316,15 @@ def other_configs(dev, prm) -> dict:
         return e0.elapsed_time(e1) / 2, out
 
     res = {}
+    # the headline slot in the strict mode (FP64 anneal, bit-identical to the
+    # reference kernel): the precision the fp32 headline is held against
+    Hh, yh, nvh, sdh, truthh = headline_slot(dev)
+    ms, r = timed(lambda: batched.detect_cim_batch(Hh, yh, nvh, ORDER, sdh,
+                                                   dataclasses.replace(prm, precision="fp64_exact")))
+    res["cfg3_16x16_16qam_slot_fp64_exact"] = {
+        "ms_per_slot": ms, "detections_per_s": P / ms * 1e3,
+        "ser": (r.x_idx != truthh).any(-1).float().mean().item()}
+    del Hh, yh, nvh, sdh, truthh
     H, y, nv, sd, truth, _ = _synthetic_uplink(dev, P, 8, 16, 20.0, 11)
     ms, r = timed(lambda: batched.detect_cim_batch(H, y, nv, 16, sd, prm))
     res["cfg2_8x8_16qam_slot"] = {"ms_per_slot": ms, "detections_per_s": P / ms * 1e3,
@@ -296,6 +350,14 @@ def other_configs(dev, prm) -> dict:
                           "ser": (r.x_idx != truth).any(-1).float().mean().item()}
     res["cfg5_16x16_64qam_30db_replica_sweep_per_slot"] = sweep
     return res
+
+
+def host_gray_bits(x_idx: np.ndarray, bpd: int) -> np.ndarray:
+    """Gray labels idx ^ (idx >> 1) of the level indices, unpacked MSB first
+    per dimension (il_gray_demap's layout) -- the e2e step's host output."""
+    g = x_idx ^ (x_idx >> 1)
+    sh = np.arange(bpd - 1, -1, -1, dtype=np.uint8)
+    return ((g[..., None] >> sh) & 1).reshape(*x_idx.shape[:-1], 2 * bpd)
 
 
 def stage_bytes(n_r: int, n_t: int, n_anneals: int) -> dict:
@@ -375,37 +437,18 @@ def run_ours(args) -> None:
     P = hi - lo
 
     # ---- synthetic slot (identical on every rank), sliced to the shard ----
-    gen = torch.Generator(device=dev).manual_seed(MASTER_SEED)
-    H = torch.complex(torch.randn(P_all, N_R, N_T, dtype=torch.float64, device=dev, generator=gen),
-                      torch.randn(P_all, N_R, N_T, dtype=torch.float64, device=dev, generator=gen))
-    H *= math.sqrt(0.5)
-    m = int(math.isqrt(ORDER))
-    levels = (torch.arange(-(m - 1), m, 2, dtype=torch.float64, device=dev)
-              / math.sqrt(2 * (m * m - 1) / 3))
-    sym_re = torch.randint(0, m, (P_all, N_T), device=dev, generator=gen)
-    sym_im = torch.randint(0, m, (P_all, N_T), device=dev, generator=gen)
-    x = torch.complex(levels[sym_re], levels[sym_im])
-    s2 = N_T / 10 ** (SNR_DB / 10)
-    noise = torch.complex(torch.randn(P_all, N_R, dtype=torch.float64, device=dev, generator=gen),
-                          torch.randn(P_all, N_R, dtype=torch.float64, device=dev, generator=gen))
-    y = torch.einsum("prt,pt->pr", H, x) + noise * math.sqrt(s2 / 2)
-    nv = torch.full((P_all,), s2, dtype=torch.float64, device=dev)
-    parts = np.stack([np.full(P_all, MASTER_SEED), np.full(P_all, 1), np.zeros(P_all),
-                      np.arange(P_all), np.full(P_all, 3)], axis=1).astype(np.uint64)
-    seeds = batched.derive_seeds(parts)  # detector seed of RE t: derive_seed(seed, 1, 0, t, 3)
-    H, y, nv, seeds = (H[lo:hi].contiguous(), y[lo:hi].contiguous(), nv[lo:hi].contiguous(),
-                       seeds[lo:hi].contiguous())
-    truth = torch.stack([sym_re[lo:hi], sym_im[lo:hi]], -1).to(torch.uint8)
-    del x, noise, sym_re, sym_im
+    H, y, nv, seeds, truth = headline_slot(dev, lo, hi)
     prm = CacParams(precision=args.precision)
-    bpd = int(round(math.log2(m)))
+    bpd = int(round(math.log2(math.isqrt(ORDER))))
 
     def step():
+        # one slot: detection, then the spin-to-bit demapper (Gray bits are
+        # the step's output); N > 1: the bits are gathered to rank 0
         r = batched.detect_cim_batch(H, y, nv, ORDER, seeds, prm)
+        bits = batched.gray_demap(r.x_idx, bpd)
         if world > 1:
-            bits = batched.gray_demap(r.x_idx, bpd)
-            gather_to_rank0(bits, shard)
-        return r
+            bits = gather_to_rank0(bits, shard)  # the slot's bits on rank 0, None elsewhere
+        return r, bits
 
     def barrier():
         if world > 1:
@@ -413,9 +456,12 @@ def run_ours(args) -> None:
         torch.cuda.synchronize()
 
     for _ in range(args.warmup):
-        res = step()
+        res, bits0 = step()
     barrier()
     ser = (res.x_idx != truth).any(-1).float().mean().item()
+    dump = os.environ.get("ISINGLINK_BENCH_BITS")  # test hook: the slot's Gray bits
+    if dump and rank == 0:
+        np.save(dump, bits0.cpu().numpy())
 
     # ---- timed region: device-resident ----
     clocks = ClockSampler(local)
@@ -463,10 +509,15 @@ def run_ours(args) -> None:
         h2d += d2h_bits.numel()  # the decided indices go back up for the bit gather
 
     def finish(r):
+        # the host-buffer entry returns level indices; their Gray bits are
+        # the step's output (numpy on the host, the reference's bit_errors
+        # semantics, channel.py:160-180), gathered to rank 0 when N > 1
         if world > 1:
             d2h_bits.copy_(r.x_idx, non_blocking=True)
             gather_to_rank0(batched.gray_demap(d2h_bits, bpd), shard)
             torch.cuda.current_stream().synchronize()
+        else:
+            host_gray_bits(r.x_idx.numpy(), bpd)
 
     def e2e_step():
         finish(batched.detect_cim_host(Hh, yh, nvh, ORDER, sh, prm, out=out_h))
@@ -563,7 +614,9 @@ def run_ours(args) -> None:
         "roofline": {"bound": "fp32", "kernel": "k_anneal_fast",
                      "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                      "frac": (achieved / fp32_peak) if achieved else None,
-                     "peak_source": "measured FFMA probe on this GPU (MEASURED_PEAKS.json has no FP32 entry)",
+                     "peak_source": "measured FP32 FMA probe on this GPU, best of FFMA and packed "
+                                    "FFMA2 (the Euler update's instruction); MEASURED_PEAKS.json "
+                                    "has no FP32 entry",
                      "flops_per_detection_fp32_pipe": f_ew, "flops_per_detection_mvm_tensor": f_mvm,
                      "mvm_tflops_on_tensor_cores": mvm_tf,
                      "anneal_ms_per_launch": an_ms / max(an_n, 1),

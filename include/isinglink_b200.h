@@ -70,6 +70,21 @@ enum il_source { IL_SRC_GUESS = 0, IL_SRC_ANNEAL = 1, IL_SRC_SIC = 2, IL_SRC_FAI
 const char* il_last_error(void);
 int il_abi_version(void);
 
+/* Which anneal kernel the batched entries run for n_dim spins per half
+ * (N = 2 n_t), n_anneals replicas and these parameters (no GPU work):
+ * IL_KERNEL_EXACT (FP64, bit-identical; always for IL_PREC_FP64_EXACT),
+ * IL_KERNEL_FAST (FP32 + tensor cores, N a multiple of 8),
+ * IL_KERNEL_FAST_PADDED (the same with inert padding spins up to the next
+ * built layout), IL_KERNEL_UMMA (tcgen05 coupling product, opt-in), or a
+ * negative IL_ERR_* for invalid parameters. */
+enum il_anneal_kernel {
+    IL_KERNEL_EXACT = 0,
+    IL_KERNEL_FAST = 1,
+    IL_KERNEL_FAST_PADDED = 2,
+    IL_KERNEL_UMMA = 3
+};
+int il_anneal_kernel(int32_t n_dim, const il_cac_params* prm);
+
 /* ---------------------------------------------------------------------------
  * Kernel plugin: replaces `_kernel.run_anneals` (_kernel.pyx:16-102, contract
  * _kernel_py.py:24-92).  G[n_dim*n_dim], g_diag[n_dim], b[n_dim],
@@ -131,8 +146,9 @@ int il_build_ising_batch(const double* H, const double* y, const uint8_t* guess_
  *     best_spins[P*(2N+1)], best_energy[P], best_index[P] (-1 when every
  *     anneal diverged or best_energy + offset > fallback_energy, i.e. when
  *     the reference returns None), diverged_count[P].  eps[P] is the
- *     resolved coupling.  steps/mvms [P*n_anneals] (optional) request the
- *     FP64-exact kernel, whose halting step is part of its contract.
+ *     resolved coupling.  steps/mvms [P*n_anneals] (optional): the
+ *     reference's per-anneal counters (steps before halting, coupling
+ *     refreshes), reported in every precision (they do not change it).
  * ------------------------------------------------------------------------- */
 int il_spin_energies(const double* G, const double* g_diag, const double* b,
                      const int8_t* spins, int64_t P, int32_t n_batch, int32_t n_dim,
@@ -246,7 +262,7 @@ int il_precode_vpp_host(const double* H, const double* u, int64_t P, int32_t n_u
 /* ---------------------------------------------------------------------------
  * Batched downlink vector-perturbation precoding: P x precode_vpp
  * (precoder.py:93-146).  H [P, n_u, n_ant] complex128 (n_u <= n_ant),
- * u [P, n_u] complex128 symbols, power P_tot > 0, tau, n_stages >= 1,
+ * u [P, n_u] complex128 symbols, power P_tot > 0, tau, 0 <= n_stages <= 15,
  * seed[p].  Outputs x[P*n_ant] complex128 transmit vector, v[P*n_u]
  * complex128 perturbation (even Gaussian integers), unnorm_power[P],
  * diverged_count[P] (may be NULL).

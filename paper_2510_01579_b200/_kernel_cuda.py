@@ -37,7 +37,12 @@ def _f64(name: str, arr, ndim: int) -> np.ndarray:
 
 def run_anneals(G, g_diag, b, x0, dt, p, a, zeta, eps, e_floor, f_mvm, n_steps,
                 diverge_threshold):
-    """Integrate a batch of anneals; returns (spins, diverged, steps, mvms)."""
+    """Integrate a batch of anneals; returns (spins, diverged, steps, mvms).
+
+    In a worker forked from a process that had initialised CUDA (the
+    reference harness's fork pools, harness/workers.py:36-38) the call is
+    served by a per-worker server process with its own CUDA context
+    (_plugin_server.py); the arithmetic and the outputs are the same."""
     G = _f64("G", G, 2)
     g_diag = _f64("g_diag", g_diag, 1)
     b = _f64("b", b, 1)
@@ -46,6 +51,11 @@ def run_anneals(G, g_diag, b, x0, dt, p, a, zeta, eps, e_floor, f_mvm, n_steps,
     n_batch, n_spins = x0.shape
     if G.shape != (n, n) or g_diag.shape[0] < n or b.shape[0] < n or n_spins != 2 * n + 1:
         raise ValueError("inconsistent problem dimensions")
+    if _lib.forked_from_cuda():
+        from . import _plugin_server
+        return _plugin_server.client().run_anneals(
+            G, g_diag, b, x0, float(dt), float(p), float(a), float(zeta), float(eps),
+            float(e_floor), int(f_mvm), int(n_steps), float(diverge_threshold))
     spins = np.empty((n_batch, n_spins), dtype=np.int8)
     diverged = np.zeros(n_batch, dtype=np.uint8)
     steps = np.full(n_batch, n_steps, dtype=np.int64)

@@ -36,6 +36,7 @@ class CacParamsC(ctypes.Structure):
 _SIGS = {
     "il_last_error": ([], ctypes.c_char_p),
     "il_abi_version": ([], ctypes.c_int),
+    "il_anneal_kernel": ([_c_i32, ctypes.POINTER(CacParamsC)], ctypes.c_int),
     "il_run_anneals": ([_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_d, _c_d, _c_d, _c_d, _c_d, _c_d,
                         _c_i32, _c_i32, _c_d, _vp, _vp, _vp, _vp, _vp], ctypes.c_int),
     "il_run_anneals_host": ([_vp, _vp, _vp, _vp, _c_i32, _c_i32, _c_d, _c_d, _c_d, _c_d, _c_d,
@@ -122,7 +123,44 @@ def check(rc: int) -> None:
 
 
 def call(name: str, *args) -> None:
+    global _used
+    _used = True
     check(getattr(load(), name)(*args))
+
+
+# ---- fork awareness --------------------------------------------------------
+# CUDA cannot be used in a child forked from a process that has initialised
+# it.  The reference's harness forks worker pools (harness/workers.py:36-38),
+# so the kernel plugin must notice the case: a child forked after the parent
+# made library calls (or initialised CUDA through torch) is flagged, and the
+# plugin routes its calls to a freshly exec'd server process instead
+# (_plugin_server.py).  A child forked before any CUDA use initialises its
+# own context lazily, like any process.
+_used = False
+_forked_from_cuda = False
+
+
+def _after_fork_in_child() -> None:
+    global _used, _forked_from_cuda, _lib
+    torch_mod = __import__("sys").modules.get("torch")
+    torch_cuda = False
+    if torch_mod is not None:
+        try:
+            torch_cuda = bool(torch_mod.cuda.is_initialized())
+        except Exception:  # pragma: no cover - torch without CUDA support
+            torch_cuda = False
+    _forked_from_cuda = _forked_from_cuda or _used or torch_cuda
+    _used = False
+
+
+if hasattr(os, "register_at_fork"):
+    os.register_at_fork(after_in_child=_after_fork_in_child)
+
+
+def forked_from_cuda() -> bool:
+    """True in a process forked from one that had initialised CUDA: this
+    process must not call the library directly."""
+    return _forked_from_cuda
 
 
 PROFILE_KINDS = ("front", "anneal", "select", "other")
@@ -149,3 +187,15 @@ def fp32_peak_tflops(reps: int = 5) -> float:
     out = ctypes.c_double(0.0)
     check(load().il_probe_fp32_peak(int(reps), ctypes.addressof(out)))
     return float(out.value)
+
+
+ANNEAL_KERNELS = {0: "exact", 1: "fast", 2: "fast_padded", 3: "umma"}
+
+
+def anneal_kernel(n_dim: int, params=None, precision: str | None = None) -> str:
+    """Name of the anneal kernel the batched entries run for n_dim spins per
+    half (il_anneal_kernel): "exact", "fast", "fast_padded" or "umma"."""
+    from .params import CacParams, to_c
+    rc = load().il_anneal_kernel(int(n_dim), to_c(params or CacParams(), precision))
+    check(min(rc, 0))
+    return ANNEAL_KERNELS[rc]

@@ -127,6 +127,16 @@ class HostTicket:
             pass
 
 
+def _host_seeds(seeds, P: int) -> torch.Tensor:
+    """Seeds as a contiguous host tensor of P 64-bit words (the C pipelines
+    copy 8 P bytes from it, so a narrower dtype is rejected, not read past)."""
+    st = seeds if isinstance(seeds, torch.Tensor) else torch.from_numpy(
+        np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1)))
+    if st.dtype not in (torch.uint64, torch.int64):
+        raise TypeError("seeds must be uint64 (or int64 bit patterns)")
+    return _host(st, st.dtype, (P,))
+
+
 def detect_cim_host_submit(H, y, noise_var, order: int, seeds, params=None,
                            precision: str | None = None, n_chunks: int = 0,
                            out=None) -> HostTicket:
@@ -143,11 +153,7 @@ def detect_cim_host_submit(H, y, noise_var, order: int, seeds, params=None,
     Hh = _host(Ht, torch.complex128, (P, n_r, n_t))
     yh = _host(y, torch.complex128, (P, n_r))
     sh = _host(noise_var, torch.float64, (P,))
-    st = seeds if isinstance(seeds, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1)))
-    if st.dtype not in (torch.uint64, torch.int64):
-        raise TypeError("seeds must be uint64 (or int64 bit patterns)")
-    st = _host(st, st.dtype, (P,))
+    st = _host_seeds(seeds, P)
     if out is None:
         pin = torch.cuda.is_available()
         out = DetectBatch(x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8, pin_memory=pin),
@@ -220,9 +226,7 @@ def precode_vpp_host(H, u, power: float, tau: float, seeds, params=None, n_stage
     P, n_u, n_ant = Ht.shape
     Hh = _host(Ht, torch.complex128, (P, n_u, n_ant))
     uh = _host(u, torch.complex128, (P, n_u))
-    st = seeds if isinstance(seeds, torch.Tensor) else torch.from_numpy(
-        np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64).reshape(-1)))
-    st = _host(st, st.dtype, (P,))
+    st = _host_seeds(seeds, P)
     pin = torch.cuda.is_available()
     out = PrecodeBatch(x=torch.empty((P, n_ant), dtype=torch.complex128, pin_memory=pin),
                        v=torch.empty((P, n_u), dtype=torch.complex128, pin_memory=pin),
@@ -456,7 +460,7 @@ class SolveBatch:
     best_energy: torch.Tensor    # f64 [P] Ising energy of the best survivor (inf if none)
     best_index: torch.Tensor     # int32 [P]; -1 where the reference returns None
     diverged: torch.Tensor       # int32 [P]
-    steps: torch.Tensor | None = None  # int64 [P, B] (FP64-exact only)
+    steps: torch.Tensor | None = None  # int64 [P, B] (counts=True; every precision)
     mvms: torch.Tensor | None = None
 
 

@@ -6,6 +6,10 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <mutex>
+
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
 
@@ -25,19 +29,75 @@ int fail_cuda(cudaError_t e, const char* what) {
     return IL_ERR_CUDA;
 }
 
-static void keep_pool_memory() {
-    static bool done = false;
-    if (done) return;
+// The library's own stream-ordered memory pool, one per device.  Its
+// settings stay private (co-located cudaMallocAsync users of the default
+// pool are unaffected):
+//   * freed workspace is kept for the next call (release threshold = max);
+//   * no stream waits on another stream's free (internal dependencies off):
+//     with streamed slots on several streams that serialised them into
+//     15-50 ms stalls;
+//   * the working set is reserved once (ISINGLINK_POOL_RESERVE_MB, default
+//     IL_POOL_RESERVE_MB, at most a quarter of the free memory; 0 = none), so
+//     that no call grows the pool: growth blocks the enqueueing thread for
+//     10-100 ms.
+#ifndef IL_POOL_RESERVE_MB
+#define IL_POOL_RESERVE_MB 6144
+#endif
+static constexpr int kMaxDevices = 64;
+
+int device_pool(cudaMemPool_t* out) {
+    static std::once_flag once[kMaxDevices];
+    static cudaMemPool_t pools[kMaxDevices];
+    static cudaError_t errs[kMaxDevices];
     int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    done = true;
+    IL_CHECK_CUDA(cudaGetDevice(&dev));
+    IL_REQUIRE(dev >= 0 && dev < kMaxDevices, "device ordinal out of range");
+    std::call_once(once[dev], [dev] {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaError_t e = cudaMemPoolCreate(&pools[dev], &props);
+        if (e == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            int no = 0;
+            e = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+            if (e == cudaSuccess)
+                e = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolReuseAllowInternalDependencies, &no);
+        }
+        if (e == cudaSuccess) {
+            const char* env = getenv("ISINGLINK_POOL_RESERVE_MB");
+            const long long mb = env && *env ? atoll(env) : (long long)IL_POOL_RESERVE_MB;
+            size_t free_b = 0, total_b = 0;
+            if (mb > 0 && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+                const size_t reserve = std::min<size_t>((size_t)mb << 20, free_b / 4);
+                cudaStream_t s = nullptr;
+                void* p = nullptr;
+                if (reserve && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess) {
+                    if (cudaMallocFromPoolAsync(&p, reserve, pools[dev], s) == cudaSuccess)
+                        cudaFreeAsync(p, s);
+                    cudaStreamSynchronize(s);
+                    cudaStreamDestroy(s);
+                }
+                cudaGetLastError();  // a failed reserve only costs the growth later
+            }
+        }
+        errs[dev] = e;
+    });
+    if (errs[dev] != cudaSuccess) return fail_cuda(errs[dev], "cudaMemPoolCreate");
+    *out = pools[dev];
+    return IL_OK;
 }
 
-Workspace::Workspace(cudaStream_t s) : st(s) { keep_pool_memory(); }
+int pool_alloc(void** p, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool;
+    const int rc = device_pool(&pool);
+    if (rc) return rc;
+    const cudaError_t e = cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, st);
+    return e == cudaSuccess ? IL_OK : fail_cuda(e, "cudaMallocFromPoolAsync");
+}
+
+Workspace::Workspace(cudaStream_t s) : st(s) {}
 
 Workspace::~Workspace() {
     for (int i = 0; i < n; ++i) cudaFreeAsync(ptrs[i], st);
@@ -64,9 +124,11 @@ int make_qam_alphabet(int order, Alphabet* out) {
 }
 
 int make_lattice_alphabet(int reach, Alphabet* out) {
-    // precoder.py:79-90: levels 4 * {-reach..reach}, spacing 4
-    if (reach < 1 || 2 * reach + 1 > 32) {
-        set_error("VPP n_stages must be in [1, 15], got %d", reach);
+    // precoder.py:79-90: levels 4 * {-reach..reach}, spacing 4.  reach = 0
+    // (n_stages = 0) is the single level 0: no stage runs and v = 0.
+    if (reach < 0 || 2 * reach + 1 > 31) {
+        set_error("VPP n_stages must be in [0, 15] (the lattice of 2 n_stages + 1 levels per "
+                  "dimension is built up to 31 levels), got %d", reach);
         return IL_ERR_ARG;
     }
     out->m = 2 * reach + 1;
@@ -159,6 +221,17 @@ extern "C" {
 
 const char* il_last_error(void) { return il::g_err; }
 int il_abi_version(void) { return IL_ABI_VERSION; }
+
+int il_anneal_kernel(int32_t n_dim, const il_cac_params* prm) {
+    int rc = validate(prm);
+    if (rc) return rc;
+    IL_REQUIRE(n_dim >= 1, "n_dim must be >= 1");
+    if (prm->precision == IL_PREC_FP64_EXACT) return IL_KERNEL_EXACT;
+    const int B = fast_rows(prm->n_anneals);
+    if (!fast_anneal_supported(n_dim, B, scalars_of(prm))) return IL_KERNEL_EXACT;
+    if (fast_anneal_uses_umma(n_dim, B)) return IL_KERNEL_UMMA;
+    return fast_anneal_layout(n_dim) == n_dim ? IL_KERNEL_FAST : IL_KERNEL_FAST_PADDED;
+}
 
 int il_run_anneals(const double* G, const double* g_diag, const double* b, const double* x0,
                    int32_t n_dim, int32_t n_batch, double dt, double p, double a, double zeta,

@@ -91,18 +91,33 @@ struct FastLayout {
 // enters the update as e*C, so storing e_s = e * 2^-sc and C_s = C * 2^sc
 // leaves e*C unchanged, and e' = max(floor, e r) becomes
 // e_s' = max(floor * 2^-sc, e_s r) -- power-of-two scalings are exact.
-template <int NT, bool SPLIT, bool SAME_QR>
+//
+// PAD: the problems have n_rt < N spins per half (any n_rt, e.g. odd n_t or
+// n_t = 20, 28).  The register layout stays that of N; spins n_rt..N-1 of
+// each half are inert: zero rows and columns of G, zero g and b, and an
+// initial state of exactly 0, which the dynamics keep at 0 (x' = x q + e C
+// with x = C = 0), so they neither couple nor diverge.  Global memory is
+// addressed with n_rt (G [n_rt][n_rt], spins [2 n_rt + 1]), and the initial
+// states are the same stream draws as for an unpadded problem of n_rt spins.
+// The PAD instantiations also serve the instrumented calls: with steps_out
+// non-null they count, per anneal, the steps before the first divergence
+// (the reference's `steps`, _kernel.pyx:85-97) and the coupling refreshes
+// (`mvms`), for the first s.b_out rows of each problem ([P][b_out] layout).
+template <int NT, bool SPLIT, bool SAME_QR, bool PAD>
 __global__ void __launch_bounds__(kWarpsPerCta * 32,
                                   (NT <= 2 ? IL_FAST_MINB2 : (NT <= 4 ? IL_FAST_MINB : 1)) * 4 / kWarpsPerCta)
 k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
               const double* __restrict__ ball, const uint64_t* __restrict__ base_seed,
               const double* __restrict__ eps_p, int64_t n_tasks, int tiles_per_prob,
               FastScalars s, int8_t* __restrict__ spins, uint8_t* __restrict__ diverged,
-              double* __restrict__ energies, bool screened) {
+              double* __restrict__ energies, bool screened, int n_rt,
+              int64_t* __restrict__ steps_out, int64_t* __restrict__ mvms_out) {
     using L = FastLayout<NT>;
     constexpr int N = L::N;
     constexpr int S = L::S;
     constexpr int KT = L::KT;
+    const int nr = PAD ? n_rt : N;  // spins per half in global memory
+    const int Sg = 2 * nr + 1;       // spins per anneal in global memory
     // scaled state (IL_SCALED_X): x~ = sqrt(dt) x wherever x is stored
     constexpr bool SC = IL_SCALED_X && SAME_QR;
     extern __shared__ __align__(16) uint4 smem_u4[];
@@ -115,9 +130,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     const int g = lane >> 2, t = lane & 3;
     const int hown = t & 1;  // the aux spin of anneal g + 8*hown is integrated by this lane
 
-    const double* G = Gall + prob * (int64_t)N * N;
-    const double* gv_p = gall + prob * N;
-    const double* bv_p = ball + prob * N;
+    const double* G = Gall + prob * (int64_t)nr * nr;
+    const double* gv_p = gall + prob * nr;
+    const double* bv_p = ball + prob * nr;
     if (!valid) return;
     uint4* frag = smem_u4 + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
     float* x0s = reinterpret_cast<float*>(frag);    // x0 staging [16][S]
@@ -129,12 +144,25 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         Pcg64 rng;
         rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)a));
         // lane part 1 jumps ahead over the first half of the stream
-        constexpr int S0 = (S + 1) / 2;
         if (part) rng.state = add128(mul128(rng.state, s.jump_mult[3]), mul128(rng.inc, s.jump_add[3]));
-        const int i0 = part ? S0 : 0, i1 = part ? S : S0;
-        for (int i = i0; i < i1; ++i)
-            x0s[al * S + i] = SC ? (float)(s.sdt * rng.uniform(s.x0_lo, s.x0_range))
-                                 : (float)rng.uniform(s.x0_lo, s.x0_range);
+        if constexpr (PAD) {
+            // stream draw i -> padded position (half A, half B, aux); the
+            // inert positions start at exactly 0
+            float* row = x0s + al * S;
+            for (int i = nr + part; i < N; i += 2) row[i] = row[N + i] = 0.f;
+            const int S0 = (Sg + 1) / 2;
+            const int i0 = part ? S0 : 0, i1 = part ? Sg : S0;
+            for (int i = i0; i < i1; ++i) {
+                const double u = rng.uniform(s.x0_lo, s.x0_range);
+                row[i < nr ? i : (i < 2 * nr ? N + i - nr : 2 * N)] = SC ? (float)(s.sdt * u) : (float)u;
+            }
+        } else {
+            constexpr int S0 = (S + 1) / 2;
+            const int i0 = part ? S0 : 0, i1 = part ? S : S0;
+            for (int i = i0; i < i1; ++i)
+                x0s[al * S + i] = SC ? (float)(s.sdt * rng.uniform(s.x0_lo, s.x0_range))
+                                     : (float)rng.uniform(s.x0_lo, s.x0_range);
+        }
     }
 
     // ---- per-problem scale 2^sc for -K*G ------------------------------------
@@ -143,17 +171,17 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     if (screened) {
         double mag = 0.0;  // sum |G| + sum |b|: the screen bound, parked in shared memory
 #pragma unroll 4
-        for (int i = lane; i < N * N; i += 32) {
+        for (int i = lane; i < nr * nr; i += 32) {
             const double v = fabs(__ldg(G + i));
             gmax = fmax(gmax, v);
             mag += v;
         }
-        for (int i = lane; i < N; i += 32) mag += fabs(bv_p[i]);
+        for (int i = lane; i < nr; i += 32) mag += fabs(bv_p[i]);
         mag = warp_sum(mag);
         if (lane == 0) reinterpret_cast<double*>(frag + L::kKgF4 - 1)[0] = mag;
     } else {
 #pragma unroll 4
-        for (int i = lane; i < N * N; i += 32) gmax = fmax(gmax, fabs(__ldg(G + i)));
+        for (int i = lane; i < nr * nr; i += 32) gmax = fmax(gmax, fabs(__ldg(G + i)));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
@@ -198,7 +226,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const int r = 16 * kt + 2 * t + (q & 1) + 8 * (q >> 1);
-                f[q] = r < N ? (float)(-Ks * __ldg(G + r * N + c)) : 0.f;
+                f[q] = (r < nr && c < nr) ? (float)(-Ks * __ldg(G + r * nr + c)) : 0.f;
             }
             uint32_t h01, l01, h23, l23;
             split_h2(make_float2(f[0], f[1]), h01, l01);
@@ -211,10 +239,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     // Euler update's scheduling instead)
     float4* kgs = reinterpret_cast<float4*>(frag + L::kKgF4);
 #pragma unroll
-    for (int n = 0; n < NT; ++n) {
-        const int i = 8 * n + 2 * t;
-        kgs[n * 32 + lane] = make_float4((float)(Ks * gv_p[i]), (float)(Ks * gv_p[i + 1]),
-                                         (float)(-Ks * bv_p[i]), (float)(-Ks * bv_p[i + 1]));
+    for (int nt = 0; nt < NT; ++nt) {
+        const int i = 8 * nt + 2 * t;
+        const double g0 = i < nr ? gv_p[i] : 0.0, g1 = i + 1 < nr ? gv_p[i + 1] : 0.0;
+        const double b0 = i < nr ? bv_p[i] : 0.0, b1 = i + 1 < nr ? bv_p[i + 1] : 0.0;
+        kgs[nt * 32 + lane] = make_float4((float)(Ks * g0), (float)(Ks * g1),
+                                          (float)(-Ks * b0), (float)(-Ks * b1));
     }
     auto kg4 = [&](int n) {
         float4 r;
@@ -229,6 +259,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     };
     __syncwarp();
 
+    // PAD + counts: iterations whose incoming states were all below the
+    // threshold (sticky tracking, so the count stops at the first divergence)
+    [[maybe_unused]] int cnt[2] = {0, 0};
+    const bool counting = PAD && steps_out != nullptr;
     int until_refresh = 0;
 #pragma unroll kStepUnroll
     for (int step = 0; step < s.n_steps; ++step) {
@@ -351,6 +385,16 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             euler_one_sc(xa, ea, Ca, s.alpha, e_floor, dva);
         else
             euler_one<SAME_QR>(xa, ea, Ca, s, e_floor, dva);
+        if constexpr (PAD) {
+            if (counting) {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float d = SC ? min_nan(dv[h][0], dv[h][1]) : max_nan(dv[h][0], dv[h][1]);
+                    if (h == hown) d = SC ? min_nan(d, dva) : max_nan(d, dva);
+                    cnt[h] += SC ? (d >= s.qthr) : (d <= s.thr2);
+                }
+            }
+        }
         --until_refresh;
     }
 
@@ -385,7 +429,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         float d = dvh[h];
         uint64_t pm = 0, nm = 0;
         const int64_t row = row0 + g + 8 * h;
-        int8_t* sp = spins + row * S;
+        int8_t* sp = spins + row * Sg;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
             d = dfold(d, xA[h][n].x, xA[h][n].y);
@@ -393,12 +437,27 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             const int i = 8 * n + 2 * t;
             const int a0 = xA[h][n].x >= 0.f ? 1 : -1, a1 = xA[h][n].y >= 0.f ? 1 : -1;
             const int b0 = xB[h][n].x >= 0.f ? 1 : -1, b1 = xB[h][n].y >= 0.f ? 1 : -1;
-            sp[i] = (int8_t)a0;
-            sp[i + 1] = (int8_t)a1;
-            sp[N + i] = (int8_t)b0;
-            sp[N + i + 1] = (int8_t)b1;
-            pm |= (uint64_t)(a0 + b0 == 2) << i | (uint64_t)(a1 + b1 == 2) << (i + 1);
-            nm |= (uint64_t)(a0 + b0 == -2) << i | (uint64_t)(a1 + b1 == -2) << (i + 1);
+            if constexpr (!PAD) {
+                sp[i] = (int8_t)a0;
+                sp[i + 1] = (int8_t)a1;
+                sp[N + i] = (int8_t)b0;
+                sp[N + i + 1] = (int8_t)b1;
+                pm |= (uint64_t)(a0 + b0 == 2) << i | (uint64_t)(a1 + b1 == 2) << (i + 1);
+                nm |= (uint64_t)(a0 + b0 == -2) << i | (uint64_t)(a1 + b1 == -2) << (i + 1);
+            } else {  // inert spins are neither stored nor part of the configuration
+                if (i < nr) {
+                    sp[i] = (int8_t)a0;
+                    sp[nr + i] = (int8_t)b0;
+                    pm |= (uint64_t)(a0 + b0 == 2) << i;
+                    nm |= (uint64_t)(a0 + b0 == -2) << i;
+                }
+                if (i + 1 < nr) {
+                    sp[i + 1] = (int8_t)a1;
+                    sp[nr + i + 1] = (int8_t)b1;
+                    pm |= (uint64_t)(a1 + b1 == 2) << (i + 1);
+                    nm |= (uint64_t)(a1 + b1 == -2) << (i + 1);
+                }
+            }
         }
         d = dmerge(d, __shfl_xor_sync(0xffffffffu, d, 1));
         d = dmerge(d, __shfl_xor_sync(0xffffffffu, d, 2));
@@ -408,9 +467,21 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         nm |= __shfl_xor_sync(0xffffffffu, nm, 2);
         pos[h] = pm;
         neg[h] = nm;
-        if (t == h) sp[2 * N] = xa >= 0.f ? 1 : -1;
+        if (t == h) sp[2 * nr] = xa >= 0.f ? 1 : -1;
         dflag[h] = SC ? !(d >= s.qthr) : !(d <= s.thr2);
         if (t == 0) diverged[row] = dflag[h] ? 1 : 0;
+        if constexpr (PAD) {
+            if (counting) {
+                int c = cnt[h];
+                c = min(c, __shfl_xor_sync(0xffffffffu, c, 1));
+                c = min(c, __shfl_xor_sync(0xffffffffu, c, 2));
+                const int a = mt * 16 + g + 8 * h;
+                if (t == 0 && a < s.b_out) {
+                    steps_out[prob * s.b_out + a] = c;
+                    mvms_out[prob * s.b_out + a] = (c + s.f_mvm - 1) / s.f_mvm;
+                }
+            }
+        }
     }
     if (screened) {
         // Selection screen: E + 2 tr G in FP32 from the tensor cores.  u =
@@ -477,7 +548,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         double* w = reinterpret_cast<double*>(frag);  // fragments are consumed
         __syncwarp();
         double tr = 0.0;
-        for (int i = lane; i < N; i += 32) tr += G[(int64_t)i * N + i];
+        for (int i = lane; i < nr; i += 32) tr += G[(int64_t)i * nr + i];
         tr = warp_sum(tr);
         while (cand) {
             const int l = __ffs(cand) - 1;
@@ -486,17 +557,18 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             const bool cax = __shfl_sync(0xffffffffu, my_aux, l);
             // E = u'Gu - 2 tr G + 2 s_aux b'u with u = 2 w (solver.py:171-175);
             // lane i sums row i through column i of the symmetric G
-            for (int j = lane; j < N; j += 32)
+            for (int j = lane; j < N; j += 32)  // (inert spins: w = 0)
                 w[j] = (double)((int)((cp >> j) & 1u) - (int)((cn >> j) & 1u));
             __syncwarp();
             double q = 0.0, li = 0.0;
-            for (int i = lane; i < N; i += 32) {
+            for (int i = lane; i < nr; i += 32) {
                 double gu[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
                 for (int j = 0; j < N; j += 4)
 #pragma unroll
                     for (int r = 0; r < 4; ++r)
-                        gu[r] = fma(__ldg(G + (int64_t)(j + r) * N + i), w[j + r], gu[r]);
+                        if (!PAD || j + r < nr)
+                            gu[r] = fma(__ldg(G + (int64_t)(j + r) * nr + i), w[j + r], gu[r]);
                 q = fma(w[i], (gu[0] + gu[1]) + (gu[2] + gu[3]), q);
                 li = fma(bv_p[i], w[i], li);
             }
@@ -519,13 +591,17 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     double rs[2][2 * NT];
 #pragma unroll
     for (int k = 0; k < 2 * NT; ++k) rs[0][k] = rs[1][k] = 0.0;
-    for (int j = 0; j < N; ++j) {
+    for (int j = 0; j < nr; ++j) {
         const double s0 = (double)((int)((pos[0] >> j) & 1u) - (int)((neg[0] >> j) & 1u));
         const double s1 = (double)((int)((pos[1] >> j) & 1u) - (int)((neg[1] >> j) & 1u));
-        const double* Gj = G + (int64_t)j * N + 2 * t;
+        const double* Gj = G + (int64_t)j * nr + 2 * t;
 #pragma unroll
         for (int n = 0; n < NT; ++n) {
-            const double2 gv = __ldg(reinterpret_cast<const double2*>(Gj + 8 * n));
+            // (PAD: rows of odd length are not 16-byte aligned; inert columns read 0)
+            const int c = 8 * n + 2 * t;
+            const double2 gv = !PAD ? __ldg(reinterpret_cast<const double2*>(Gj + 8 * n))
+                                    : make_double2(c < nr ? __ldg(Gj + 8 * n) : 0.0,
+                                                   c + 1 < nr ? __ldg(Gj + 8 * n + 1) : 0.0);
             rs[0][2 * n] = fma(gv.x, s0, rs[0][2 * n]);
             rs[0][2 * n + 1] = fma(gv.y, s0, rs[0][2 * n + 1]);
             rs[1][2 * n] = fma(gv.x, s1, rs[1][2 * n]);
@@ -542,10 +618,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             const double si1 = (double)((int)((pos[1] >> i) & 1u) - (int)((neg[1] >> i) & 1u));
             quad[0] = fma(si0, rs[0][2 * n + dl], quad[0]);
             quad[1] = fma(si1, rs[1][2 * n + dl], quad[1]);
-            const double bi = bg[i];
-            lin[0] = fma(bi, si0, lin[0]);
-            lin[1] = fma(bi, si1, lin[1]);
-            tr += G[(int64_t)i * N + i];
+            if (!PAD || i < nr) {
+                const double bi = bg[i];
+                lin[0] = fma(bi, si0, lin[0]);
+                lin[1] = fma(bi, si1, lin[1]);
+                tr += G[(int64_t)i * nr + i];
+            }
         }
     }
 #pragma unroll
@@ -563,40 +641,61 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     }
 }
 
-template <int NT, bool SPLIT, bool SAME_QR>
+template <int NT, bool SPLIT, bool SAME_QR, bool PAD>
 int launch_cfg(const double* G, const double* g, const double* b, const uint64_t* base_seed,
                const double* eps_p, int64_t n_tasks, int tiles, const FastScalars& fs,
-               int8_t* spins, uint8_t* diverged, double* energies, bool screened,
-               cudaStream_t st) {
+               int8_t* spins, uint8_t* diverged, double* energies, bool screened, int n_rt,
+               int64_t* steps, int64_t* mvms, cudaStream_t st) {
     const int64_t blocks = (n_tasks + kWarpsPerCta - 1) / kWarpsPerCta;
     IL_REQUIRE(blocks < (1ll << 31), "too many problems in one launch");
     const size_t smem = FastLayout<NT>::kWarpBytes;
-    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR>;
+    auto fn = k_anneal_fast<NT, SPLIT, SAME_QR, PAD>;
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     IL_LAUNCH(kProfAnneal, st, fn<<<(unsigned)blocks, kWarpsPerCta * 32, smem, st>>>(G, g, b, base_seed, eps_p, n_tasks, tiles,
-                                                        fs, spins, diverged, energies, screened););
+                                                        fs, spins, diverged, energies, screened, n_rt, steps, mvms););
     IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
+}
+
+template <int NT, bool PAD>
+int launch_pad(const double* G, const double* g, const double* b, const uint64_t* base_seed,
+               const double* eps_p, int64_t n_tasks, int tiles, const FastScalars& fs, bool split,
+               bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, bool screened,
+               int n_rt, int64_t* steps, int64_t* mvms, cudaStream_t st) {
+    if (split) {
+        return same_qr ? launch_cfg<NT, true, true, PAD>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                        spins, diverged, energies, screened, n_rt, steps, mvms, st)
+                       : launch_cfg<NT, true, false, PAD>(G, g, b, base_seed, eps_p, n_tasks, tiles,
+                                                         fs, spins, diverged, energies, screened, n_rt, steps, mvms, st);
+    }
+    return same_qr ? launch_cfg<NT, false, true, PAD>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                     spins, diverged, energies, screened, n_rt, steps, mvms, st)
+                   : launch_cfg<NT, false, false, PAD>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
+                                                      spins, diverged, energies, screened, n_rt, steps, mvms, st);
 }
 
 template <int NT>
 int launch_nt(const double* G, const double* g, const double* b, const uint64_t* base_seed,
               const double* eps_p, int64_t P, int B, const FastScalars& fs, bool split,
               bool same_qr, int8_t* spins, uint8_t* diverged, double* energies, bool screened,
-              cudaStream_t st) {
+              int n_rt, int64_t* steps, int64_t* mvms, cudaStream_t st) {
     const int tiles = B / 16;
     const int64_t n_tasks = P * tiles;
-    if (split) {
-        return same_qr ? launch_cfg<NT, true, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                   spins, diverged, energies, screened, st)
-                       : launch_cfg<NT, true, false>(G, g, b, base_seed, eps_p, n_tasks, tiles,
-                                                    fs, spins, diverged, energies, screened, st);
-    }
-    return same_qr ? launch_cfg<NT, false, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                spins, diverged, energies, screened, st)
-                   : launch_cfg<NT, false, false>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs,
-                                                 spins, diverged, energies, screened, st);
+    if (n_rt == 8 * NT && steps == nullptr)
+        return launch_pad<NT, false>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs, split, same_qr,
+                                     spins, diverged, energies, screened, n_rt, steps, mvms, st);
+    return launch_pad<NT, true>(G, g, b, base_seed, eps_p, n_tasks, tiles, fs, split, same_qr,
+                                spins, diverged, energies, screened, n_rt, steps, mvms, st);
+}
+
+// Register layouts built: N = 8 NT spins per half for these NT; a problem of
+// n spins runs on the smallest N >= n (inert padding spins, see k_anneal_fast).
+constexpr int kFastNT[] = {1, 2, 3, 4, 6, 8};
+int fast_nt_for(int n) {
+    for (int nt : kFastNT)
+        if (8 * nt >= n) return nt;
+    return 0;
 }
 
 }  // namespace
@@ -613,8 +712,12 @@ static bool use_umma() {
     return v != 0;
 }
 
+bool fast_anneal_uses_umma(int N, int B) { return use_umma() && umma_anneal_supported(N, B); }
+
+int fast_anneal_layout(int N) { return 8 * fast_nt_for(N); }
+
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
-    if (N % 8 != 0 || N < 8 || N > 64 || B % 16 != 0 || B <= 0) return false;
+    if (N < 1 || fast_nt_for(N) == 0 || B % 16 != 0 || B <= 0) return false;
     // the aux/initial-state check folds x0 into the sticky max: require |x0| < thr
     if (!(s.x0_range * 0.5 < s.thr)) return false;
     // e may not overflow FP32 while x stays below the threshold
@@ -629,7 +732,8 @@ bool fast_anneal_supported(int N, int B, const AnnealScalars& s) {
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st, int screen_rows) {
+                       double* energies, cudaStream_t st, int screen_rows, int64_t* steps,
+                       int64_t* mvms, int count_rows) {
     if (!fast_anneal_supported(N, B, s)) {
         set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
         return IL_ERR_UNSUPPORTED;
@@ -650,6 +754,9 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.sdt = sqrt(s.dt);
     fs.qthr = (float)(1.0 + s.dt * (s.p - 1.0) - s.dt * s.thr * s.thr);
     fs.b_valid = screen_rows;
+    fs.b_out = count_rows;
+    IL_REQUIRE((steps == nullptr) == (mvms == nullptr) && (!steps || (count_rows > 0 && count_rows <= B)),
+               "fast anneal: steps and mvms go together, for 1..B rows");
     // the screen pays off from N = 24 on (at N = 16 the FP64 epilogue is cheaper)
     // ISINGLINK_SCREEN=0 turns the screen off (the parity test compares both)
     static const bool screen_on = [] {
@@ -657,7 +764,7 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
         return !(e && *e == '0');
     }();
     const bool screened = screen_on && screen_rows > 0 && N >= 24;
-    for (int k = 0; k < 3; ++k) pcg_jump((k + 1) * ((2 * N + 1 + 3) / 4), &fs.jump_mult[k], &fs.jump_add[k]);
+    // lane part 1 of an anneal's two x0 lanes starts (2N + 2) / 2 draws into the stream
     pcg_jump((2 * N + 2) / 2, &fs.jump_mult[3], &fs.jump_add[3]);
     const bool split = precision != IL_PREC_TF32;
     // x and e share their per-step factor exactly when zeta*dt == dt and
@@ -668,12 +775,12 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     // thresholds) take the general instantiation, which compares x^2 directly.
     const bool same_qr = fs.alpha == fs.beta && fs.ndt == fs.ndtz &&
                          (!IL_SCALED_X || s.dt * s.thr * s.thr >= fabs((double)fs.alpha) * 0x1p-6);
-    if (use_umma() && umma_anneal_supported(N, B))
+    if (use_umma() && steps == nullptr && umma_anneal_supported(N, B))
         return launch_anneal_umma(G, g, b, base_seed, eps_p, P, N, B, &fs, split, same_qr, spins,
                                   diverged, energies, screened, st);
 #define IL_NT(k) \
-    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, st)
-    switch (N / 8) {
+    case k: return launch_nt<k>(G, g, b, base_seed, eps_p, P, B, fs, split, same_qr, spins, diverged, energies, screened, N, steps, mvms, st)
+    switch (fast_nt_for(N)) {
         IL_NT(1);
         IL_NT(2);
         IL_NT(3);

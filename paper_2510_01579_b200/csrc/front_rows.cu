@@ -463,7 +463,7 @@ int launch_rows_gs(const double* H, const double* y, const double* s2, int64_t P
     const int64_t blocks = (P + groups - 1) / groups;
     cplx* scratch = nullptr;
     if (M && I && IL_FRONT_SAVE_A)
-        IL_CHECK_CUDA(cudaMallocAsync((void**)&scratch, sizeof(cplx) * GS * GS * (size_t)P, st));
+        if (const int rc = pool_alloc((void**)&scratch, sizeof(cplx) * GS * GS * (size_t)P, st)) return rc;
     IL_LAUNCH(kProfFront, st, fn<<<(unsigned)blocks, kRowsThreads, smem, st>>>(H, y, s2, P, n_r, n, al, x_idx, energy, status, o, scratch););
     const cudaError_t e = cudaGetLastError();
     if (scratch) cudaFreeAsync(scratch, st);

@@ -29,11 +29,12 @@ struct FastScalars {
     float thr2;     // diverge_threshold^2
     double dt;
     double x0_lo, x0_range;
-    U128 jump_mult[4], jump_add[4];  // PCG64 advance by 1, 2, 3 quarter segments; [3]: half
+    U128 jump_mult[4], jump_add[4];  // [3]: PCG64 advance by half a stream ([0..2] unused)
     int f_mvm, n_steps;
     double sdt;   // sqrt(dt): scale of the stored state (IL_SCALED_X)
     float qthr;   // alpha - dt thr^2: q below it means |x| > thr (IL_SCALED_X)
     int b_valid;  // anneal rows per problem that enter the selection (screened energies)
+    int b_out;    // anneal rows per problem whose steps / mvms are counted (PAD + counts)
 };
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }

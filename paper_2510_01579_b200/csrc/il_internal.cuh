@@ -20,10 +20,11 @@ int launch_anneal_exact(const double* G, const double* g, const double* b, const
                         const AnnealScalars& s, int8_t* spins, uint8_t* diverged,
                         int64_t* steps, int64_t* mvms, cudaStream_t st);
 
-// FP32 state + tensor-core coupling product.  Requires N % 8 == 0 (N <= 64),
-// B % 16 == 0.  Divergence is a sticky flag (spins of diverged anneals are
-// not frozen: they never enter selection).  Returns IL_ERR_UNSUPPORTED when
-// the shape is not instantiated.
+// FP32 state + tensor-core coupling product.  Requires 1 <= N <= 64 (N not
+// a multiple of 8 runs with inert padding spins), B % 16 == 0.  Divergence
+// is a sticky flag (spins of diverged anneals are not frozen: they never
+// enter selection).  steps / mvms (optional, [P][count_rows]): per-anneal
+// step and refresh counts as the reference kernel reports them.
 // Energies: the FP64 energy of every anneal; or, with screen_rows > 0, only of
 // the anneals among the first screen_rows rows of each problem that can be the
 // FP64 argmin of those rows (+inf for the others): an FP32 tensor-core
@@ -33,8 +34,13 @@ int launch_anneal_exact(const double* G, const double* g, const double* b, const
 int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
-                       double* energies, cudaStream_t st, int screen_rows = 0);
+                       double* energies, cudaStream_t st, int screen_rows = 0,
+                       int64_t* steps = nullptr, int64_t* mvms = nullptr, int count_rows = 0);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
+// launch_anneal_fast hands the shape to the tcgen05 kernel (opt-in)
+bool fast_anneal_uses_umma(int N, int B);
+// spins per half of the register layout the FP32 kernel runs N on (>= N; 0: none)
+int fast_anneal_layout(int N);
 // The same anneal with the coupling product on tcgen05 (anneal_umma.cu);
 // launch_anneal_fast dispatches to it when enabled and supported.
 bool umma_anneal_supported(int N, int B);
@@ -162,7 +168,11 @@ void prof_stop(int idx, cudaStream_t st);
         ::il::prof_stop(_pi, (st));                       \
     } while (0)
 
-// ---- workspace (stream-ordered pool allocations) ----------------------------
+// ---- workspace (stream-ordered allocations from the library's pool) --------
+// pool_alloc: cudaMallocFromPoolAsync from the library's private per-device
+// pool (abi.cu); the memory is released with cudaFreeAsync.
+int pool_alloc(void** p, size_t bytes, cudaStream_t st);
+
 struct Workspace {
     cudaStream_t st;
     void* ptrs[32];
@@ -178,11 +188,8 @@ struct Workspace {
             return nullptr;
         }
         void* p = nullptr;
-        cudaError_t e = cudaMallocAsync(&p, count ? count * sizeof(T) : 1, st);
-        if (e != cudaSuccess) {
-            *rc = fail_cuda(e, "cudaMallocAsync(workspace)");
-            return nullptr;
-        }
+        *rc = pool_alloc(&p, count * sizeof(T), st);
+        if (*rc != IL_OK) return nullptr;
         ptrs[n++] = p;
         return static_cast<T*>(p);
     }

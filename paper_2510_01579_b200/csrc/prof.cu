@@ -52,6 +52,22 @@ __global__ void k_ffma_probe(float* out, float s, int iters) {
     for (int i = 0; i < 8; ++i) r += a[i];
     if (r == 1234.5f) out[0] = r;
 }
+// The same with packed FFMA2 (two FMAs per instruction), which the anneal's
+// Euler update issues: 8 chains x 2 lanes = 16 FMAs per iteration.
+__global__ void k_ffma2_probe(float* out, float s, int iters) {
+    float2 a[8];
+    const float2 b = make_float2(s * threadIdx.x, s * threadIdx.x + 0.25f), c = make_float2(s + 1.f, s + 0.5f);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = make_float2(s * i, s * i + 0.125f);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(a[i], b, c);
+    }
+    float r = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r += a[i].x + a[i].y;
+    if (r == 1234.5f) out[0] = r;
+}
 }  // namespace
 
 }  // namespace il
@@ -95,7 +111,9 @@ int il_profile_end(double* ms_by_kind, long long* launches_by_kind, int n_kinds)
     return IL_OK;
 }
 
-// Dense FFMA throughput of this GPU (TFLOP/s), best of `reps` launches.
+// Dense FP32 FMA throughput of this GPU (TFLOP/s): the best of `reps`
+// launches each of an FFMA and an FFMA2 (packed) probe -- the roofline
+// denominator is the faster of the two instructions the anneal issues.
 int il_probe_fp32_peak(int reps, double* tflops) {
     float* out = nullptr;
     IL_CHECK_CUDA(cudaMalloc(&out, 4));
@@ -106,17 +124,25 @@ int il_probe_fp32_peak(int reps, double* tflops) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    il::k_ffma_probe<<<blocks, threads>>>(out, 0.5f, iters);
     double best = 0.0;
-    for (int r = 0; r < (reps < 1 ? 1 : reps); ++r) {
-        cudaEventRecord(a);
-        il::k_ffma_probe<<<blocks, threads>>>(out, 0.5f, iters);
-        cudaEventRecord(b);
-        cudaEventSynchronize(b);
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, a, b);
-        const double fl = 2.0 * 8.0 * iters * (double)blocks * threads;
-        if (ms > 0) best = fmax(best, fl / (ms * 1e-3) / 1e12);
+    for (int packed = 0; packed < 2; ++packed) {
+        auto launch = [&] {
+            if (packed)
+                il::k_ffma2_probe<<<blocks, threads>>>(out, 0.5f, iters);
+            else
+                il::k_ffma_probe<<<blocks, threads>>>(out, 0.5f, iters);
+        };
+        launch();  // warm-up
+        for (int r = 0; r < (reps < 1 ? 1 : reps); ++r) {
+            cudaEventRecord(a);
+            launch();
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, a, b);
+            const double fl = 2.0 * 8.0 * (packed ? 2.0 : 1.0) * iters * (double)blocks * threads;
+            if (ms > 0) best = fmax(best, fl / (ms * 1e-3) / 1e12);
+        }
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);

@@ -138,17 +138,21 @@ int il_solve_batch(const double* G, const double* g_diag, const double* b, const
     s.n_steps = prm->n_steps;
     int rc = IL_OK;
     Workspace ws(st);
+    // counters (steps / mvms) are reported by both kernels, so asking for
+    // them does not change the arithmetic (the precision alone selects it)
     const bool want_counts = steps != nullptr || mvms != nullptr;
-    const bool fast = !want_counts && prm->precision != IL_PREC_FP64_EXACT &&
+    const bool fast = prm->precision != IL_PREC_FP64_EXACT &&
                       fast_anneal_supported(N, fast_rows(B), s);
     const int Bs = fast ? fast_rows(B) : B;  // padded rows are never selected
     int8_t* spins = ws.get<int8_t>((size_t)P * Bs * S, &rc);
     uint8_t* div = ws.get<uint8_t>((size_t)P * Bs, &rc);
     double* en = ws.get<double>((size_t)P * Bs, &rc);
+    if (want_counts && !steps) steps = ws.get<int64_t>((size_t)P * B, &rc);
+    if (want_counts && !mvms) mvms = ws.get<int64_t>((size_t)P * B, &rc);
     if (rc) return rc;
     if (fast) {
         rc = launch_anneal_fast(G, g_diag, b, base_seed, eps, P, N, Bs, s, prm->precision, spins,
-                                div, en, st);
+                                div, en, st, 0, steps, mvms, B);
         if (rc) return rc;
     } else {
         rc = launch_anneal_exact(G, g_diag, b, nullptr, base_seed, eps, P, N, B, s, spins, div, steps,

@@ -26,9 +26,6 @@ using namespace il;
 #ifndef IL_PIPE_IDLE_CHUNKS
 #define IL_PIPE_IDLE_CHUNKS 12
 #endif
-#ifndef IL_POOL_RESERVE_MB  // memory-pool reserve for streamed slots
-#define IL_POOL_RESERVE_MB 6144
-#endif
 #ifndef IL_PIPE_TAPER  // halve the last chunks (env ISINGLINK_PIPE_TAPER=2 on, 1 off)
 #define IL_PIPE_TAPER 0
 #endif
@@ -64,35 +61,6 @@ struct Streams {
 
 std::mutex g_pipe_mu;
 Streams g_pipe[64];  // per device ordinal
-
-void keep_pool_warm() {
-    static bool done = false;
-    if (done) return;
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;  // keep freed workspace for the next call
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        // never let the allocator make a stream wait on another stream's free:
-        // with slots in flight on several streams that serialises them
-        int no = 0;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &no);
-        // ... and reserve its working set once (freed, kept by the threshold
-        // above), so that no call has to grow the pool: growth blocks the
-        // enqueueing thread for milliseconds (measured 10-100 ms stalls)
-        size_t free_b = 0, total_b = 0;
-        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-            const size_t reserve = std::min<size_t>((size_t)IL_POOL_RESERVE_MB << 20, free_b / 4);
-            void* p = nullptr;
-            if (reserve && cudaMallocAsync(&p, reserve, 0) == cudaSuccess) {
-                cudaFreeAsync(p, 0);
-                cudaStreamSynchronize(0);
-            }
-            cudaGetLastError();
-        }
-    }
-    done = true;
-}
 
 // One per-item array moved between host and device: `bytes` per problem.
 struct PipeBuf {
@@ -155,7 +123,6 @@ std::vector<int64_t> chunk_bounds(int64_t P, int n_chunks) {
 template <class F>
 int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& compute,
                  cudaEvent_t* done = nullptr) {
-    keep_pool_warm();
     static const bool trace = env_int("ISINGLINK_PIPE_TRACE", 0) > 0;
     const auto t_start = std::chrono::steady_clock::now();
     int dev_id = 0;
@@ -179,8 +146,7 @@ int run_pipeline(int64_t P, int n_chunks, std::vector<PipeBuf>& bufs, F&& comput
     if (rc) return rc;
     for (PipeBuf& b : bufs) {  // stream-ordered on `in`, published by the first event
         if (rc) break;
-        cudaError_t e = cudaMallocAsync((void**)&b.dev, b.bytes * P, ss.in);
-        if (e != cudaSuccess) rc = fail_cuda(e, "cudaMallocAsync(pipeline)");
+        rc = pool_alloc((void**)&b.dev, b.bytes * P, ss.in);
     }
     // ISINGLINK_PIPE_TRACE=2: per-chunk device timeline (timing events)
     std::vector<cudaEvent_t> tev;

@@ -45,3 +45,21 @@ def test_cubin_is_sm100a(built_lib):
     out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True,
                          text=True).stdout
     assert "sm_100a" in out
+
+
+def test_anneal_kernel_routing_is_host_only(built_lib):
+    """il_anneal_kernel answers without touching the GPU: every n_t <= 32
+    runs the FP32 kernel in the throughput modes (inert padding spins when
+    N = 2 n_t is not a built layout), the exact mode always the FP64 kernel."""
+    from paper_2510_01579_b200 import _lib
+    from paper_2510_01579_b200.params import CacParams
+    for n_t in range(1, 33):
+        N = 2 * n_t
+        want = "fast" if N in (8, 16, 24, 32, 48, 64) else "fast_padded"
+        assert _lib.anneal_kernel(N, CacParams()) == want, N
+        assert _lib.anneal_kernel(N, CacParams(), "tf32") == want, N
+        assert _lib.anneal_kernel(N, CacParams(), "fp64_exact") == "exact"
+    assert _lib.anneal_kernel(66, CacParams()) == "exact"  # beyond the FP32 layouts
+    import pytest
+    with pytest.raises(ValueError):
+        _lib.anneal_kernel(8, CacParams(dt=-1.0))

@@ -243,14 +243,20 @@ class TestDetect:
             agree += np.array_equal(o["x"], res.x_hard)
         assert agree / 40 >= (1.0 if precision == "fp64_exact" else 0.95)
 
-    def test_counters_path_equals_fused_path(self):
-        for trial in range(8):
+    @pytest.mark.parametrize("precision", ["fp64_exact", "fp32", "tf32"])
+    def test_counters_path_equals_fused_path(self, precision):
+        """Counters are instrumentation: passing them runs the same arithmetic
+        (the precision alone selects the kernel) and returns the same result."""
+        for trial in range(12):
             inst = random_instance(8, 8, 16, 15.0, tag=4001, trial=trial)
             c = {}
-            a = api.detect_cim(inst, CacParams(precision="fp64_exact"), seed=trial, counters=c)
-            b = api.detect_cim(inst, CacParams(precision="fp64_exact"), seed=trial)
+            a = api.detect_cim(inst, CacParams(precision=precision), seed=trial, counters=c)
+            b = api.detect_cim(inst, CacParams(precision=precision), seed=trial)
             assert np.array_equal(a.x_hard, b.x_hard) and a.source == b.source
+            assert a.energy == b.energy and a.anneal_index == b.anneal_index
+            assert a.diverged_count == b.diverged_count == c["diverged"]
             assert c["anneals"] == 32 and c["mvm_updates"] >= 64 * (32 - c["diverged"])
+            assert c["steps"] >= 128 * (32 - c["diverged"])
 
     def test_all_anneals_divergent_returns_mmse(self):
         inst = random_instance(4, 4, 4, 15.0, tag=4004)
@@ -268,12 +274,19 @@ class TestDetect:
         assert (a.energy, a.source, a.anneal_index, a.diverged_count) == (
             b.energy, b.source, b.anneal_index, b.diverged_count)
 
-    def test_odd_shapes_take_exact_fallback(self):
+    def test_odd_shapes_run_padded_fast_kernel(self):
+        """n_t = 3, 6, 9 (N = 6, 12, 18 spins per half, not multiples of 8)
+        run the FP32 kernel with inert padding spins; the exact mode still
+        reproduces the oracle, the FP32 mode decides the same on these."""
+        from paper_2510_01579_b200 import _lib
         for (nr, nt) in ((5, 3), (12, 6), (9, 9)):
+            assert _lib.anneal_kernel(2 * nt, CacParams()) == "fast_padded"
             inst = random_instance(nr, nt, 16, 18.0, tag=4010 + nt)
-            res = api.detect_cim(inst, CacParams(), seed=1)
             o = orc.detect_cim(inst.H, inst.y, inst.noise_var, 16, seed=1)
-            assert np.array_equal(res.x_hard, o["x"])
+            ex = api.detect_cim(inst, CacParams(precision="fp64_exact"), seed=1)
+            assert np.array_equal(ex.x_hard, o["x"])
+            fa = api.detect_cim(inst, CacParams(), seed=1)
+            assert fa.energy <= ex.energy * (1 + 1e-12)
 
 
 def downlink_draw(tag, trial, n=4, order=16):
