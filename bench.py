@@ -352,14 +352,6 @@ def other_configs(dev, prm) -> dict:
     return res
 
 
-def host_gray_bits(x_idx: np.ndarray, bpd: int) -> np.ndarray:
-    """Gray labels idx ^ (idx >> 1) of the level indices, unpacked MSB first
-    per dimension (il_gray_demap's layout) -- the e2e step's host output."""
-    g = x_idx ^ (x_idx >> 1)
-    sh = np.arange(bpd - 1, -1, -1, dtype=np.uint8)
-    return ((g[..., None] >> sh) & 1).reshape(*x_idx.shape[:-1], 2 * bpd)
-
-
 def stage_bytes(n_r: int, n_t: int, n_anneals: int) -> dict:
     """Algorithmic HBM bytes per RE of the streaming stages (complex128 H, y
     as the reference holds them; FP64 G, g, b out; int8 spins in)."""
@@ -488,39 +480,43 @@ def run_ours(args) -> None:
     value = P_all * args.steps / (ms_max / 1e3)
 
     # ---- e2e: pinned host buffers through the host-buffer C-ABI entry ----
-    # il_detect_cim_host streams the shard through the GPU in chunks with the
-    # H2D copy of the inputs, the detection and the D2H copy of every output
-    # overlapped; all copies are inside the timed region.
+    # il_detect_cim_bits_host_submit streams the shard through the GPU in
+    # chunks with the H2D copy of the inputs, the detection, the Gray
+    # demapper and the D2H copy of every output (bits, level indices,
+    # energies, sources, winners, divergence counts) overlapped; all copies
+    # are inside the timed region.
     Hh = H.cpu().pin_memory()
     yh = y.cpu().pin_memory()
     nvh = nv.cpu().pin_memory()
     sh = seeds.cpu().pin_memory()
-    out_h = batched.DetectBatch(
-        x_idx=torch.empty((P, N_T, 2), dtype=torch.uint8).pin_memory(),
-        energy=torch.empty(P, dtype=torch.float64).pin_memory(),
-        source=torch.empty(P, dtype=torch.int8).pin_memory(),
-        anneal_index=torch.empty(P, dtype=torch.int32).pin_memory(),
-        diverged=torch.empty(P, dtype=torch.int32).pin_memory())
+    def host_outputs():
+        return batched.DetectBatch(
+            x_idx=torch.empty((P, N_T, 2), dtype=torch.uint8).pin_memory(),
+            energy=torch.empty(P, dtype=torch.float64).pin_memory(),
+            source=torch.empty(P, dtype=torch.int8).pin_memory(),
+            anneal_index=torch.empty(P, dtype=torch.int32).pin_memory(),
+            diverged=torch.empty(P, dtype=torch.int32).pin_memory(),
+            bits=torch.empty((P, N_T, 2 * bpd), dtype=torch.uint8).pin_memory())
+
+    out_h = host_outputs()
     h2d = Hh.numel() * 16 + yh.numel() * 16 + nvh.numel() * 8 + sh.numel() * 8
     d2h = sum(t.numel() * t.element_size() for t in
-              (out_h.x_idx, out_h.energy, out_h.source, out_h.anneal_index, out_h.diverged))
+              (out_h.x_idx, out_h.energy, out_h.source, out_h.anneal_index, out_h.diverged,
+               out_h.bits))
     if world > 1:
-        d2h_bits = torch.empty((P, N_T, 2), dtype=torch.uint8, device=dev)
-        h2d += d2h_bits.numel()  # the decided indices go back up for the bit gather
+        dev_bits = torch.empty((P, N_T, 2 * bpd), dtype=torch.uint8, device=dev)
+        h2d += dev_bits.numel()  # the host bits go back up for the NCCL gather
 
     def finish(r):
-        # the host-buffer entry returns level indices; their Gray bits are
-        # the step's output (numpy on the host, the reference's bit_errors
-        # semantics, channel.py:160-180), gathered to rank 0 when N > 1
+        # the step's output is the Gray bits in host memory; with N > 1 they
+        # are gathered to rank 0
         if world > 1:
-            d2h_bits.copy_(r.x_idx, non_blocking=True)
-            gather_to_rank0(batched.gray_demap(d2h_bits, bpd), shard)
+            dev_bits.copy_(r.bits, non_blocking=True)
+            gather_to_rank0(dev_bits, shard)
             torch.cuda.current_stream().synchronize()
-        else:
-            host_gray_bits(r.x_idx.numpy(), bpd)
 
     def e2e_step():
-        finish(batched.detect_cim_host(Hh, yh, nvh, ORDER, sh, prm, out=out_h))
+        finish(batched.detect_cim_host(Hh, yh, nvh, ORDER, sh, prm, out=out_h, bits=True))
 
     def e2e_timed(streamed: bool) -> float:
         """ms for args.steps slots; streamed: slot s+1 is submitted before
@@ -531,7 +527,7 @@ def run_ours(args) -> None:
             prev = None
             for k in range(args.steps):
                 tk = batched.detect_cim_host_submit(Hh, yh, nvh, ORDER, sh, prm,
-                                                    out=outs[k % 2])
+                                                    out=outs[k % 2], bits=True)
                 if prev is not None:
                     finish(prev.wait())
                 prev = tk
@@ -545,24 +541,22 @@ def run_ours(args) -> None:
             dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         return float(ms.item())
 
-    outs = [out_h, batched.DetectBatch(
-        x_idx=torch.empty((P, N_T, 2), dtype=torch.uint8).pin_memory(),
-        energy=torch.empty(P, dtype=torch.float64).pin_memory(),
-        source=torch.empty(P, dtype=torch.int8).pin_memory(),
-        anneal_index=torch.empty(P, dtype=torch.int32).pin_memory(),
-        diverged=torch.empty(P, dtype=torch.int32).pin_memory())]
+    outs = [out_h, host_outputs()]
     e2e_step()
     e2e_sync_ms = e2e_timed(False)
     # untimed warm-up of the streamed path (its workspaces are sized for the
     # two-chunk mode a slot takes while the previous one is still running)
     prev = None
     for k in range(max(args.warmup, 3)):
-        tk = batched.detect_cim_host_submit(Hh, yh, nvh, ORDER, sh, prm, out=outs[k % 2])
+        tk = batched.detect_cim_host_submit(Hh, yh, nvh, ORDER, sh, prm, out=outs[k % 2],
+                                            bits=True)
         if prev is not None:
             finish(prev.wait())
         prev = tk
     finish(prev.wait())
     e2e_ms = e2e_timed(True)
+    # the bits that left the GPU are the device step's bits
+    e2e_bits_ok = all(torch.equal(o.bits, bits0.cpu()) for o in outs) if world == 1 else None
     e2e_value = P_all * args.steps / (e2e_ms / 1e3)
     e2e_sync_value = P_all * args.steps / (e2e_sync_ms / 1e3)
 
@@ -607,8 +601,10 @@ def run_ours(args) -> None:
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args),
         "e2e": {"value": e2e_value, "unit": UNIT, "mode": "streamed: slot s+1 submitted before slot s "
-                "is waited for (il_detect_cim_host_submit); every slot's H2D and D2H in the timed region",
-                "one_slot_at_a_time": e2e_sync_value, "h2d_bytes_per_step": int(h2d),
+                "is waited for (il_detect_cim_bits_host_submit: detection + Gray demapper, bits "
+                "out); every slot's H2D and D2H in the timed region",
+                "one_slot_at_a_time": e2e_sync_value, "bits_identical_to_device_step": e2e_bits_ok,
+                "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": int(launches),
         "roofline": {"bound": "fp32", "kernel": "k_anneal_fast",

@@ -251,6 +251,19 @@ int il_detect_cim_host_submit(const double* H, const double* y, const double* no
                               int32_t* diverged_count, int32_t n_chunks, void** ticket);
 int il_pipeline_wait(void* ticket);
 
+/* il_detect_cim_host_submit plus the spin-to-bit demapper in the same
+ * pipeline: bits[P * n_t * 2 * log2(sqrt(qam_order))] receives the Gray bits
+ * of the decided symbols (il_gray_demap's layout, computed on the device per
+ * chunk), so the uplink receiver's output leaves the GPU as bits.  Every
+ * output pointer may be NULL (not copied back); x_idx NULL keeps the level
+ * indices on the device. */
+int il_detect_cim_bits_host_submit(const double* H, const double* y, const double* noise_var,
+                                   int64_t P, int32_t n_r, int32_t n_t, int32_t qam_order,
+                                   const uint64_t* seed, const il_cac_params* prm,
+                                   uint8_t* bits, uint8_t* x_idx, double* energy,
+                                   int8_t* source, int32_t* anneal_index,
+                                   int32_t* diverged_count, int32_t n_chunks, void** ticket);
+
 /* Host-buffer form of il_precode_vpp_batch (every pointer HOST memory),
  * streamed through the device in n_chunks pieces (<= 0: auto) like
  * il_detect_cim_host. */

@@ -66,6 +66,9 @@ _SIGS = {
     "il_detect_cim_host_submit": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
                                    ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _c_i32,
                                    ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
+    "il_detect_cim_bits_host_submit": ([_vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _c_i32, _vp,
+                                        ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _vp,
+                                        _c_i32, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
     "il_pipeline_wait": ([_vp], ctypes.c_int),
     "il_precode_vpp_host": ([_vp, _vp, _c_i64, _c_i32, _c_i32, _c_d, _c_d, _c_i32, _vp,
                              ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _c_i32],

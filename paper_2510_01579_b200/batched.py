@@ -61,6 +61,7 @@ class DetectBatch:
     source: torch.Tensor         # int8 [P]  0 guess (MMSE), 1 anneal, -1 failed
     anneal_index: torch.Tensor   # int32 [P] winning anneal or -1
     diverged: torch.Tensor       # int32 [P] diverged anneal count
+    bits: torch.Tensor | None = None  # uint8 [P, n_t, 2 bpd] Gray bits (host entries, bits=True)
 
 
 def detect_cim_batch(H, y, noise_var, order: int, seeds, params=None,
@@ -139,11 +140,12 @@ def _host_seeds(seeds, P: int) -> torch.Tensor:
 
 def detect_cim_host_submit(H, y, noise_var, order: int, seeds, params=None,
                            precision: str | None = None, n_chunks: int = 0,
-                           out=None) -> HostTicket:
+                           out=None, bits: bool = False) -> HostTicket:
     """Streaming form of ``detect_cim_host`` (il_detect_cim_host_submit):
     enqueue the slot and return a ticket at once.  Slots submitted back to
     back overlap: the next slot's copies and first chunks run under this
-    slot's tail."""
+    slot's tail.  bits=True also returns the Gray bits of the decisions,
+    demapped on the device inside the pipeline (il_detect_cim_bits_host_submit)."""
     params = params or CacParams()
     prm = to_c(params, precision)
     Ht = H if isinstance(H, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(H))
@@ -154,23 +156,35 @@ def detect_cim_host_submit(H, y, noise_var, order: int, seeds, params=None,
     yh = _host(y, torch.complex128, (P, n_r))
     sh = _host(noise_var, torch.float64, (P,))
     st = _host_seeds(seeds, P)
+    pin = torch.cuda.is_available()
     if out is None:
-        pin = torch.cuda.is_available()
         out = DetectBatch(x_idx=torch.empty((P, n_t, 2), dtype=torch.uint8, pin_memory=pin),
                           energy=torch.empty(P, dtype=torch.float64, pin_memory=pin),
                           source=torch.empty(P, dtype=torch.int8, pin_memory=pin),
                           anneal_index=torch.empty(P, dtype=torch.int32, pin_memory=pin),
                           diverged=torch.empty(P, dtype=torch.int32, pin_memory=pin))
     handle = ctypes.c_void_p()
-    _lib.call("il_detect_cim_host_submit", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(), P, n_r,
-              n_t, int(order), st.data_ptr(), prm, out.x_idx.data_ptr(), out.energy.data_ptr(),
-              out.source.data_ptr(), out.anneal_index.data_ptr(), out.diverged.data_ptr(),
-              int(n_chunks), ctypes.byref(handle))
+    if bits:
+        m = int(round(math.sqrt(int(order))))
+        bpd = max(1, (m - 1).bit_length())
+        if out.bits is None or tuple(out.bits.shape) != (P, n_t, 2 * bpd):
+            out.bits = torch.empty((P, n_t, 2 * bpd), dtype=torch.uint8, pin_memory=pin)
+        _lib.call("il_detect_cim_bits_host_submit", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(),
+                  P, n_r, n_t, int(order), st.data_ptr(), prm, out.bits.data_ptr(),
+                  out.x_idx.data_ptr(), out.energy.data_ptr(), out.source.data_ptr(),
+                  out.anneal_index.data_ptr(), out.diverged.data_ptr(), int(n_chunks),
+                  ctypes.byref(handle))
+    else:
+        _lib.call("il_detect_cim_host_submit", Hh.data_ptr(), yh.data_ptr(), sh.data_ptr(), P,
+                  n_r, n_t, int(order), st.data_ptr(), prm, out.x_idx.data_ptr(),
+                  out.energy.data_ptr(), out.source.data_ptr(), out.anneal_index.data_ptr(),
+                  out.diverged.data_ptr(), int(n_chunks), ctypes.byref(handle))
     return HostTicket(handle, out, (Hh, yh, sh, st))
 
 
 def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
-                    precision: str | None = None, n_chunks: int = 0, out=None) -> DetectBatch:
+                    precision: str | None = None, n_chunks: int = 0, out=None,
+                    bits: bool = False) -> DetectBatch:
     """P x ``detect_cim`` from HOST buffers to HOST buffers.
 
     The slot is streamed through the GPU in chunks with H2D copy, detection
@@ -178,7 +192,7 @@ def detect_cim_host(H, y, noise_var, order: int, seeds, params=None,
     (``tensor.pin_memory()``) for the overlap; ``out`` may hold preallocated
     (pinned) output tensors in DetectBatch layout."""
     return detect_cim_host_submit(H, y, noise_var, order, seeds, params, precision, n_chunks,
-                                  out).wait()
+                                  out, bits).wait()
 
 
 @dataclass

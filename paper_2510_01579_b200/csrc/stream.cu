@@ -231,7 +231,8 @@ namespace {
 int detect_host(const double* H, const double* y, const double* noise_var, int64_t P, int32_t n_r,
                 int32_t n_t, int32_t qam_order, const uint64_t* seed, const il_cac_params* prm,
                 uint8_t* x_idx, double* energy, int8_t* source, int32_t* anneal_index,
-                int32_t* diverged_count, int32_t n_chunks, cudaEvent_t* done);
+                int32_t* diverged_count, int32_t n_chunks, cudaEvent_t* done,
+                uint8_t* bits = nullptr);
 }
 
 extern "C" int il_detect_cim_host(const double* H, const double* y, const double* noise_var,
@@ -259,6 +260,23 @@ extern "C" int il_detect_cim_host_submit(const double* H, const double* y,
     return rc;
 }
 
+extern "C" int il_detect_cim_bits_host_submit(const double* H, const double* y,
+                                              const double* noise_var, int64_t P, int32_t n_r,
+                                              int32_t n_t, int32_t qam_order, const uint64_t* seed,
+                                              const il_cac_params* prm, uint8_t* bits,
+                                              uint8_t* x_idx, double* energy, int8_t* source,
+                                              int32_t* anneal_index, int32_t* diverged_count,
+                                              int32_t n_chunks, void** ticket) {
+    IL_REQUIRE(ticket, "ticket must not be NULL");
+    *ticket = nullptr;
+    cudaEvent_t done = nullptr;
+    const int rc = detect_host(H, y, noise_var, P, n_r, n_t, qam_order, seed, prm, x_idx, energy,
+                               source, anneal_index, diverged_count, n_chunks, &done,
+                               bits);
+    if (rc == IL_OK) *ticket = done;
+    return rc;
+}
+
 extern "C" int il_pipeline_wait(void* ticket) {
     if (!ticket) return IL_OK;
     cudaEvent_t ev = static_cast<cudaEvent_t>(ticket);
@@ -272,23 +290,36 @@ namespace {
 int detect_host(const double* H, const double* y, const double* noise_var, int64_t P, int32_t n_r,
                 int32_t n_t, int32_t qam_order, const uint64_t* seed, const il_cac_params* prm,
                 uint8_t* x_idx, double* energy, int8_t* source, int32_t* anneal_index,
-                int32_t* diverged_count, int32_t n_chunks, cudaEvent_t* done) {
+                int32_t* diverged_count, int32_t n_chunks, cudaEvent_t* done, uint8_t* bits) {
     IL_REQUIRE(P >= 0 && n_t >= 1 && n_r >= n_t && n_t <= 32,
                "uplink detection requires 1 <= n_t <= n_r, n_t <= 32");
-    IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && x_idx), "NULL buffer");
+    IL_REQUIRE(P == 0 || (H && y && noise_var && seed && prm && (x_idx || bits)), "NULL buffer");
+    int bpd = 0;  // Gray bits per PAM dimension
+    if (bits) {
+        Alphabet al;
+        const int rc = make_qam_alphabet(qam_order, &al);
+        if (rc) return rc;
+        while ((1 << bpd) < al.m) ++bpd;
+    }
     if (P == 0) return IL_OK;
+    // outputs with a NULL host pointer stay device scratch (x_idx feeds the
+    // demapper; the others are not copied back)
     std::vector<PipeBuf> b = {
         {H, nullptr, sizeof(double) * 2 * n_r * n_t}, {y, nullptr, sizeof(double) * 2 * n_r},
         {noise_var, nullptr, sizeof(double)},         {seed, nullptr, sizeof(uint64_t)},
         {nullptr, x_idx, (size_t)2 * n_t},            {nullptr, energy, sizeof(double)},
         {nullptr, source, 1},                         {nullptr, anneal_index, sizeof(int32_t)},
-        {nullptr, diverged_count, sizeof(int32_t)}};
+        {nullptr, diverged_count, sizeof(int32_t)},   {nullptr, bits, (size_t)2 * n_t * bpd}};
+    if (!bits) b.pop_back();
     return run_pipeline(P, n_chunks, b, [&](int64_t o, int64_t n, cudaStream_t cs) {
         auto at = [&](int k) { return b[k].dev + o * b[k].bytes; };
-        return il_detect_cim_batch((const double*)at(0), (const double*)at(1),
-                                   (const double*)at(2), n, n_r, n_t, qam_order,
-                                   (const uint64_t*)at(3), prm, (uint8_t*)at(4), (double*)at(5),
-                                   (int8_t*)at(6), (int32_t*)at(7), (int32_t*)at(8), cs);
+        int rc = il_detect_cim_batch((const double*)at(0), (const double*)at(1),
+                                     (const double*)at(2), n, n_r, n_t, qam_order,
+                                     (const uint64_t*)at(3), prm, (uint8_t*)at(4), (double*)at(5),
+                                     (int8_t*)at(6), (int32_t*)at(7), (int32_t*)at(8), cs);
+        if (rc == IL_OK && bits)
+            rc = launch_gray_demap((const uint8_t*)at(4), n * n_t, bpd, (uint8_t*)at(9), cs);
+        return rc;
     }, done);
 }
 }  // namespace

@@ -20,8 +20,20 @@ from isinglink import (CacParams, build_ising, derive_seed, detect_cim, detect_c
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref", "pkg_tests"))
-from conftest import random_instance  # noqa: E402  (the reference's generator)
+
+
+def _reference_conftest():
+    """The reference's tests/conftest.py, loaded by path (this repo's own
+    tests/conftest.py shadows the name on sys.path)."""
+    import importlib.util
+    path = os.path.join(ROOT, "oracle", "_ref", "pkg_tests", "conftest.py")
+    spec = importlib.util.spec_from_file_location("isinglink_ref_conftest", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+random_instance = _reference_conftest().random_instance  # the reference's generator
 
 PAIR = ("cuda", "ext")
 

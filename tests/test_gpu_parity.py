@@ -335,3 +335,24 @@ def test_precode_vpp_host_pipeline_matches_device_batch(n_chunks):
         assert torch.equal(getattr(dev, f).cpu(), getattr(host, f)), f
     n = len(d["v"])
     assert np.array_equal(host.v.numpy()[:n], d["v"])
+
+
+def test_host_pipeline_bits_equal_device_demap():
+    """il_detect_cim_bits_host_submit: the Gray bits demapped inside the host
+    pipeline equal il_gray_demap of the device batch's decisions, with or
+    without the other outputs copied back."""
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    for name, bpd in (("d16x16_16qam_20db", 2), ("d8x8_qpsk_10db", 1), ("d16x16_64qam_25db", 3)):
+        d = load_golden(f"{name}.npz")
+        reps = 9
+        H = np.concatenate([d["H"]] * reps)
+        y = np.concatenate([d["y"]] * reps)
+        s2 = np.concatenate([d["noise_var"]] * reps)
+        seed = np.concatenate([d["seed"]] * reps)
+        prm = CacParams(precision="fp32")
+        dev = batched.detect_cim_batch(H, y, s2, int(d["order"]), seed, prm)
+        want = batched.gray_demap(dev.x_idx, bpd).cpu()
+        host = batched.detect_cim_host(H, y, s2, int(d["order"]), seed, prm, n_chunks=3, bits=True)
+        assert torch.equal(host.bits, want), name
+        assert torch.equal(host.x_idx, dev.x_idx.cpu()), name

@@ -33,7 +33,7 @@ ACTIVE_FILES = ["test_solver.py", "test_transform.py", "test_detector.py", "test
                 "test_linear.py", "test_channel.py", "test_harness.py"]
 
 
-def _run(files, activate: bool, timeout=900):
+def _run(files, activate: bool, timeout=900, verbose=False):
     if not (os.path.isdir(REF_TESTS) and os.path.isdir(REF_PKG)):
         pytest.fail("reference suite not staged: run `make -C oracle refpkg` in the build "
                     "container (it needs /root/reference)")
@@ -41,7 +41,7 @@ def _run(files, activate: bool, timeout=900):
     env["PYTHONPATH"] = os.pathsep.join([os.path.join(ROOT, "tests"), ROOT,
                                          env.get("PYTHONPATH", "")])
     env["ISINGLINK_REF_ACTIVATE"] = "1" if activate else "0"
-    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "ref_suite_plugin", "-p",
+    cmd = [sys.executable, "-m", "pytest", "-v" if verbose else "-q", "-p", "ref_suite_plugin", "-p",
            "no:cacheprovider", "-c", os.devnull, "--rootdir", REF_TESTS, *files]
     r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True,
                        timeout=timeout)
@@ -52,8 +52,9 @@ def _run(files, activate: bool, timeout=900):
 
 
 def test_reference_backend_suite_with_cuda_registered(built_lib):
-    out = _run(["test_backends.py"], activate=False)
-    assert "cuda" in out  # the header lists the kernels
+    out = _run(["test_backends.py"], activate=False, verbose=True)
+    # the reference's parametrised determinism test ran on the CUDA backend
+    assert "test_each_backend_is_deterministic[cuda] PASSED" in out
 
 
 @pytest.mark.parametrize("name", ACTIVE_FILES)
