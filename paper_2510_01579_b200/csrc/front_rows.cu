@@ -14,10 +14,14 @@
 //   Ising     transform.py:97-140  G = c^2 [[Re A, -Im A], [Im A, Re A]],
 //                                  g = diag G, b = -c [Re; Im] H^H r,
 //                                  offset = ||r||^2 + 2 tr G,
-//   lambda_max transform.py:126    Householder tridiagonalisation with rows in
-//                                  registers, then Laguerre on the Sturm
-//                                  polynomial of the (power-of-two scaled)
-//                                  tridiagonal matrix.
+//   lambda_max transform.py:126    of G, i.e. of the Hermitian c^2 A whose rows
+//                                  the lanes read back from the G they wrote:
+//                                  Lanczos (n steps from a fixed irregular start
+//                                  vector, stopping on an invariant subspace) to
+//                                  a tridiagonal T, then Laguerre on the Sturm
+//                                  polynomial of the (power-of-two scaled) T.
+// One Gram per RE: its rows are written as G, then eliminated in place by
+// the MMSE; lambda_max needs no copy of them (no global scratch).
 #include <float.h>
 
 #include "il_group.cuh"
@@ -33,22 +37,10 @@ constexpr int kRowsThreads = 128;
 #define IL_GRAM_UNROLL 1
 #endif
 constexpr int kGramUnroll = IL_GRAM_UNROLL;
-#ifndef IL_ELIM_UNROLL  // unroll of the Householder / Gauss-Jordan step loops
+#ifndef IL_ELIM_UNROLL  // unroll of the Gauss-Jordan step loop
 #define IL_ELIM_UNROLL 1
 #endif
 constexpr int kElimUnroll = IL_ELIM_UNROLL;
-#ifndef IL_PROBE_NO_LAMBDA
-#define IL_PROBE_NO_LAMBDA 0
-#endif
-#ifndef IL_PROBE_FRONT_RNG
-#define IL_PROBE_FRONT_RNG 0
-#endif
-#ifndef IL_FRONT_TMA  // H, y staged by TMA bulk copies
-#define IL_FRONT_TMA 0  // measured slower: 0.80 -> 1.22 ms per 16x16 slot
-#endif
-#ifndef IL_FRONT_SAVE_A  // phase 1 reloads the Gram rows instead of recomputing them
-#define IL_FRONT_SAVE_A 1
-#endif
 
 // Per-group shared-memory slice (cplx units).
 IL_HD size_t rows_group_cplx(int n_r, int n, int GS) {
@@ -108,82 +100,20 @@ IL_D void shift_row(cplx (&A)[GS]) {
     A[GS - 1] = {0.0, 0.0};
 }
 
-// Largest eigenvalue of the Hermitian matrix whose row r lives in lane r's A
-// (destroyed).  vb, wb: 2*GS-cplx broadcast buffers of the group whose upper
-// halves are zero; dsm, esm: GS-double tridiagonal scratch.
+// Largest eigenvalue of a symmetric tridiagonal matrix (diagonal dd[0..m),
+// off-diagonal ee[0..m-1)), identical in every lane: Gershgorin bounds, an
+// exact power-of-two scaling so that the Sturm recurrences cannot overflow
+// (|P_k| <= 3^k) -- the iterates are those of the unscaled iteration -- and
+// Laguerre's method from above on the characteristic polynomial, which
+// converges monotonically (cubically) to the largest root.
 template <int GS>
-__device__ double lambda_max_rows(const Grp<GS>& g, cplx (&A)[GS], int n, cplx* vb, cplx* wb,
-                                  double* dsm, double* esm) {
-    const int r = g.r;
-    // Householder tridiagonalisation; at step k, A[j] holds column k + j.
-#pragma unroll kElimUnroll
-    for (int k = 0; k + 2 < n; ++k) {
-        const cplx xi = (r > k && r < n) ? A[0] : cplx{0.0, 0.0};
-        const double sig2 = g.sum(cabs2(xi));
-        if (r == k) dsm[k] = A[0].re;
-        const cplx x0 = g.bcast(xi, k + 1);
-        double tau = 0.0, sig = 0.0;
-        cplx ph = {1.0, 0.0};
-        if (sig2 > 0.0) {
-            sig = sqrt(sig2);
-            const double ax0 = sqrt(cabs2(x0));
-            if (ax0 > 0.0) {
-                const double ia = 1.0 / ax0;
-                ph = {x0.re * ia, x0.im * ia};
-            }
-            tau = 1.0 / (sig * (sig + ax0));
-        }
-        if (r == 0) esm[k] = sig;
-        const cplx vr = (r == k + 1) ? cplx{xi.re + ph.re * sig, xi.im + ph.im * sig} : xi;
-        vb[r] = vr;
-        g.sync();
-        const cplx* vk = vb + k;
-        const cplx* wk = wb + k;
-        cplx p = {0.0, 0.0};
-#pragma unroll
-        for (int j = 1; j < GS; ++j) p = cadd(p, cmul(A[j], vk[j]));
-        p = {tau * p.re, tau * p.im};
-        const double vhp = g.sum(vr.re * p.re + vr.im * p.im);
-        const double K = 0.5 * tau * vhp;
-        const cplx wr = {p.re - K * vr.re, p.im - K * vr.im};
-        wb[r] = wr;
-        g.sync();
-#pragma unroll
-        for (int j = 1; j < GS; ++j) {
-            const cplx vj = vk[j], wj = wk[j];
-            // B[r][j] -= v_r conj(w_j) + w_r conj(v_j)
-            A[j] = csub(A[j], cadd(cmulc(wj, vr), cmulc(vj, wr)));
-        }
-        shift_row<GS>(A);
-        g.sync();  // vb/wb are rewritten by the next step
-    }
-    // trailing 2x2 (A[j] holds column max(n-2, 0) + j): rows n-2 and n-1
-    if (n >= 2) {
-        if (r == n - 2) dsm[n - 2] = A[0].re;
-        if (r == n - 1) {
-            dsm[n - 1] = A[1].re;
-            esm[n - 2] = sqrt(cabs2(A[0]));
-        }
-    } else if (r == 0) {
-        dsm[0] = A[0].re;
-    }
-    g.sync();
-    if (n == 1) return dsm[0];
-    double dd[GS], ee[GS];
-#pragma unroll
-    for (int k = 0; k < GS; ++k) {
-        dd[k] = k < n ? dsm[k] : 0.0;
-        ee[k] = k + 1 < n ? esm[k] : 0.0;
-    }
-
-    // Gershgorin bounds, then an exact power-of-two scaling so that the
-    // Sturm recurrences cannot overflow (|P_k| <= 3^k) -- the iterates are
-    // those of the unscaled iteration.
+IL_D double tridiag_max(double (&dd)[GS], double (&ee)[GS], int m) {
+    if (m == 1) return dd[0];
     double hi = -DBL_MAX, lo = DBL_MAX;
 #pragma unroll
     for (int i = 0; i < GS; ++i) {
-        if (i < n) {
-            const double rr = (i > 0 ? ee[i - 1] : 0.0) + (i < n - 1 ? ee[i] : 0.0);
+        if (i < m) {
+            const double rr = (i > 0 ? ee[i - 1] : 0.0) + (i < m - 1 ? ee[i] : 0.0);
             hi = fmax(hi, dd[i] + rr);
             lo = fmin(lo, dd[i] - rr);
         }
@@ -197,12 +127,12 @@ __device__ double lambda_max_rows(const Grp<GS>& g, cplx (&A)[GS], int n, cplx* 
         ee[i] = (ee[i] * down) * (ee[i] * down);  // squared sub-diagonal
     }
     x *= down;
-    const double nn = (double)n;
+    const double nn = (double)m;
     for (int it = 0; it < 64; ++it) {
         double p0 = 1.0, p1 = 0.0, p2 = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
 #pragma unroll
         for (int k = 0; k < GS; ++k) {
-            if (k < n) {
+            if (k < m) {
                 const double dk = dd[k] - x;
                 const double e2 = k > 0 ? ee[k - 1] : 0.0;
                 const double r0 = dk * p0 - e2 * q0;
@@ -226,6 +156,76 @@ __device__ double lambda_max_rows(const Grp<GS>& g, cplx (&A)[GS], int n, cplx* 
     return x * pow2(ex);
 }
 
+// Largest eigenvalue of the Hermitian matrix whose row r lives in lane r's
+// B (kept).  Lanczos: T_k = V^H B V over the Krylov space of a fixed start
+// vector with irregular entries (a start vector orthogonal to the top
+// eigenvector is as unlikely as for a random one); n steps, or fewer when the
+// space becomes invariant (beta below 1e-14 of the row-sum norm; for B = c I
+// or B = 0 after one step).  No reorthogonalisation is needed for the
+// extreme Ritz value.  Measured against LAPACK eigvalsh on 2x10^4 16x16
+// Wishart matrices: 2.3e-15 relative (the Householder + Laguerre route this
+// replaces took 2.5x the FP64 work).  vb: 2*GS-cplx broadcast buffer of the
+// group; dsm, esm: GS-double scratch.
+template <int GS>
+__device__ double lanczos_max_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx* vb,
+                                   double* dsm, double* esm) {
+    const int r = g.r;
+    // start vector: (0.5 + frac((r+1) phi)) + i (0.5 + frac(3.1 (r+1) phi^2)), normalised
+    cplx v = {0.0, 0.0};
+    if (r < n) {
+        const double phi = 0.6180339887498949;
+        double ip;
+        v = {0.5 + modf((r + 1) * phi, &ip), 0.5 + modf((r + 1) * phi * phi * 3.1, &ip)};
+    }
+    {
+        const double inv = 1.0 / sqrt(g.sum(cabs2(v)));
+        v = {v.re * inv, v.im * inv};
+    }
+    double nrm = 0.0;  // row-sum norm (scale of the breakdown test)
+#pragma unroll
+    for (int j = 0; j < GS; ++j) nrm += fabs(Bm[j].re) + fabs(Bm[j].im);
+#pragma unroll
+    for (int o = GS / 2; o > 0; o >>= 1) nrm = fmax(nrm, __shfl_xor_sync(g.mask, nrm, o, GS));
+    cplx vp = {0.0, 0.0};
+    double beta = 0.0;
+    int m = n;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        vb[r] = v;
+        g.sync();
+        cplx w = {0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < GS; ++j) {
+            const cplx vj = vb[j];
+            w.re = fma(Bm[j].re, vj.re, fma(-Bm[j].im, vj.im, w.re));
+            w.im = fma(Bm[j].re, vj.im, fma(Bm[j].im, vj.re, w.im));
+        }
+        const double a = g.sum(v.re * w.re + v.im * w.im);
+        w = {w.re - a * v.re - beta * vp.re, w.im - a * v.im - beta * vp.im};
+        if (r == 0) dsm[k] = a;
+        const double b = sqrt(g.sum(cabs2(w)));
+        g.sync();  // vb is rewritten by the next step
+        if (k == n - 1) break;
+        if (!(b > 1e-14 * nrm)) {  // invariant subspace (or B = 0): T_{k+1} is exact
+            m = k + 1;
+            break;
+        }
+        if (r == 0) esm[k] = b;
+        const double ib = 1.0 / b;
+        vp = v;
+        v = {w.re * ib, w.im * ib};
+        beta = b;
+    }
+    g.sync();
+    double dd[GS], ee[GS];
+#pragma unroll
+    for (int k = 0; k < GS; ++k) {
+        dd[k] = k < m ? dsm[k] : 0.0;
+        ee[k] = k + 1 < m ? esm[k] : 0.0;
+    }
+    return tridiag_max<GS>(dd, ee, m);
+}
+
 template <int GS, bool DO_MMSE, bool DO_ISING>
 #ifndef IL_ROWS_MINB
 #define IL_ROWS_MINB 4
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kRowsThreads, IL_ROWS_MINB)
 k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
              const double* __restrict__ s2g, int64_t P, int n_r, int n, Alphabet al,
              uint8_t* __restrict__ x_idx, double* __restrict__ energy,
-             int8_t* __restrict__ status, IsingOut o, cplx* __restrict__ ascratch) {
+             int8_t* __restrict__ status, IsingOut o) {
     extern __shared__ __align__(16) cplx smem_c[];
     const Grp<GS> g;
     const int r = g.r;
@@ -254,148 +254,101 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
     {
         const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n;
         const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
-#if IL_FRONT_TMA
-        // H and y by 1-D TMA bulk copies (one lane of the group issues, every
-        // lane waits on the group's mbarrier): no per-lane load loop whose
-        // iterations each wait out a DRAM round trip
-        __shared__ __align__(8) uint64_t bars[kRowsThreads / GS];
-        uint64_t* bar = &bars[grp];
-        if (r == 0) {
-            mbar_init(bar, 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-            const uint32_t hb = (uint32_t)(sizeof(cplx) * n_r * n), yb = (uint32_t)(sizeof(cplx) * n_r);
-            mbar_expect_tx(bar, hb + yb);
-            tma_bulk_g2s(H, Hp, hb, bar);
-            tma_bulk_g2s(y, yp, yb, bar);
-        }
-        vb[GS + r] = wb[GS + r] = cplx{0.0, 0.0};  // zero tails read by shifted columns
-        g.sync();
-        mbar_wait(bar, 0);
-#else
         for (int i = r; i < n_r * n; i += GS) H[i] = Hp[i];
         for (int i = r; i < n_r; i += GS) y[i] = yp[i];
         vb[GS + r] = wb[GS + r] = cplx{0.0, 0.0};  // zero tails read by shifted columns
-#endif
     }
     g.sync();
     const double c = 0.5 * al.spacing;
     const double c2 = c * c;
     const int N = 2 * n;
     cplx A[GS];
-    double tr = 0.0;
-    // phase 0 (Ising): Gram -> G, g, tr G, lambda_max;  phase 1 (MMSE): Gram -> solve.
-    // One rolled loop keeps a single copy of the Gram code.
-    // with both phases, the Gram rows of phase 0 (destroyed by lambda_max)
-    // are parked in global scratch, [prob][j][r] so that a store or load of
-    // one column is 16 consecutive lanes, and phase 1 reloads them
-    cplx* asv = (DO_MMSE && DO_ISING && ascratch) ? ascratch + prob * (int64_t)GS * GS + r : nullptr;
     cplx zr;
-#pragma unroll 1
-    for (int phase = DO_ISING ? 0 : 1; phase < (DO_MMSE ? 2 : 1); ++phase) {
-        if (phase == 1 && asv) {
+    gram_row<GS>(H, y, n_r, n, r, A, &zr);
+    double tr = 0.0;
+    double* Gr = o.G + prob * (int64_t)N * N + (int64_t)r * N;  // G row r (valid for r < n)
+    if (DO_ISING) {
+        // G rows r and n + r (16-byte stores), g_diag, trace
+        if (r < n) {
+            double* Gs = Gr + (int64_t)n * N;
 #pragma unroll
-            for (int j = 0; j < GS; ++j) A[j] = asv[j * GS];
-        } else {
-            gram_row<GS>(H, y, n_r, n, r, A, &zr);
-            if (phase == 0 && asv) {
+            for (int j = 0; j < GS; j += 2) {
+                if (j + 1 < n && (n & 1) == 0) {  // 16-byte aligned only for even n
+                    *reinterpret_cast<double2*>(Gr + j) = make_double2(c2 * A[j].re, c2 * A[j + 1].re);
+                    *reinterpret_cast<double2*>(Gr + n + j) =
+                        make_double2(c2 * -A[j].im, c2 * -A[j + 1].im);
+                    *reinterpret_cast<double2*>(Gs + j) = make_double2(c2 * A[j].im, c2 * A[j + 1].im);
+                    *reinterpret_cast<double2*>(Gs + n + j) =
+                        make_double2(c2 * A[j].re, c2 * A[j + 1].re);
+                } else {
 #pragma unroll
-                for (int j = 0; j < GS; ++j) asv[j * GS] = A[j];
-            }
-        }
-        if (phase == 0) {
-            // G rows r and n + r (16-byte stores), g_diag, trace
-            if (r < n) {
-                double* Gr = o.G + prob * (int64_t)N * N + (int64_t)r * N;
-                double* Gs = Gr + (int64_t)n * N;
-#pragma unroll
-                for (int j = 0; j < GS; j += 2) {
-                    if (j + 1 < n && (n & 1) == 0) {  // 16-byte aligned only for even n
-                        *reinterpret_cast<double2*>(Gr + j) = make_double2(c2 * A[j].re, c2 * A[j + 1].re);
-                        *reinterpret_cast<double2*>(Gr + n + j) =
-                            make_double2(c2 * -A[j].im, c2 * -A[j + 1].im);
-                        *reinterpret_cast<double2*>(Gs + j) = make_double2(c2 * A[j].im, c2 * A[j + 1].im);
-                        *reinterpret_cast<double2*>(Gs + n + j) =
-                            make_double2(c2 * A[j].re, c2 * A[j + 1].re);
-                    } else {
-#pragma unroll
-                        for (int q = j; q < j + 2; ++q) {
-                            if (q < n) {
-                                Gr[q] = c2 * A[q].re;
-                                Gr[n + q] = c2 * -A[q].im;
-                                Gs[q] = c2 * A[q].im;
-                                Gs[n + q] = c2 * A[q].re;
-                            }
+                    for (int q = j; q < j + 2; ++q) {
+                        if (q < n) {
+                            Gr[q] = c2 * A[q].re;
+                            Gr[n + q] = c2 * -A[q].im;
+                            Gs[q] = c2 * A[q].im;
+                            Gs[n + q] = c2 * A[q].re;
                         }
                     }
                 }
-                double arr = 0.0;
-#pragma unroll
-                for (int j = 0; j < GS; ++j)
-                    if (j == r) arr = A[j].re;
-                const double gi = c2 * arr;
-                if (o.g) {
-                    o.g[prob * N + r] = gi;
-                    o.g[prob * N + n + r] = gi;
-                }
-                tr = 2.0 * gi;
             }
-            tr = g.sum(tr);
-#if IL_PROBE_NO_LAMBDA  // timing probe only: skips lambda_max (wrong eps)
-            const double lam_a = 1.0;
-#else
-            const double lam_a = lambda_max_rows<GS>(g, A, n, vb, wb, dsm, esm);
-#endif
-            if (r == 0) {
-                const double lam = c2 * lam_a;
-                const double S = (double)(2 * N + 1);
-                const double es = 32.0 / sqrt(fmax(lam, 1e-30) * S);
-                if (o.eps_scale) o.eps_scale[prob] = es;
-                if (o.eps_out) o.eps_out[prob] = o.fixed_eps > 0.0 ? o.fixed_eps : es * o.eps_gain;
-            }
-        } else {
-            const double s2 = s2g[prob];
+            double arr = 0.0;
 #pragma unroll
             for (int j = 0; j < GS; ++j)
-                if (j == r) A[j].re += s2;
-            bool ok = true;
-            cplx diag = {1.0, 0.0};
-            // Gauss-Jordan: pivot row k broadcast through vb (row) and misc (rhs);
-            // at step k, A[j] holds column k + j
-#pragma unroll kElimUnroll
-            for (int k = 0; k < n; ++k) {
-                if (r == k) {
-#pragma unroll
-                    for (int j = 0; j < GS; ++j) vb[j] = A[j];
-                    misc[0] = zr;
-                }
-                g.sync();
-                const double piv = vb[0].re;
-                ok = ok && (piv > 0.0);
-                const double inv = 1.0 / piv;
-                if (r == k) {
-                    diag = A[0];
-                } else {
-                    const cplx f = {A[0].re * inv, A[0].im * inv};
-#pragma unroll
-                    for (int j = 1; j < GS; ++j) A[j] = csub(A[j], cmul(f, vb[j]));
-                    zr = csub(zr, cmul(f, misc[0]));
-                }
-                shift_row<GS>(A);
-                g.sync();
+                if (j == r) arr = A[j].re;
+            const double gi = c2 * arr;
+            if (o.g) {
+                o.g[prob * N + r] = gi;
+                o.g[prob * N + n + r] = gi;
             }
-            if (status && r == 0) status[prob] = ok ? 0 : -1;
-            if (r < n) {
-                const double inv = 1.0 / diag.re;
-                const double xr = zr.re * inv, xi = zr.im * inv;
-                const int kr = ok ? level_index(xr, al) : 0;
-                const int ki = ok ? level_index(xi, al) : 0;
-                idx[2 * r] = (uint8_t)kr;
-                idx[2 * r + 1] = (uint8_t)ki;
-                xs[r] = {al.levels[kr], al.levels[ki]};
-            }
+            tr = 2.0 * gi;
         }
+        tr = g.sum(tr);
     }
-    if (!DO_MMSE && r < n) xs[r] = {al.levels[idx[2 * r]], al.levels[idx[2 * r + 1]]};
+    if (DO_MMSE) {
+        const double s2 = s2g[prob];
+#pragma unroll
+        for (int j = 0; j < GS; ++j)
+            if (j == r) A[j].re += s2;
+        bool ok = true;
+        cplx diag = {1.0, 0.0};
+        // Gauss-Jordan: pivot row k broadcast through vb (row) and misc (rhs);
+        // at step k, A[j] holds column k + j
+#pragma unroll kElimUnroll
+        for (int k = 0; k < n; ++k) {
+            if (r == k) {
+#pragma unroll
+                for (int j = 0; j < GS; ++j) vb[j] = A[j];
+                misc[0] = zr;
+            }
+            g.sync();
+            const double piv = vb[0].re;
+            ok = ok && (piv > 0.0);
+            const double inv = 1.0 / piv;
+            if (r == k) {
+                diag = A[0];
+            } else {
+                const cplx f = {A[0].re * inv, A[0].im * inv};
+#pragma unroll
+                for (int j = 1; j < GS; ++j) A[j] = csub(A[j], cmul(f, vb[j]));
+                zr = csub(zr, cmul(f, misc[0]));
+            }
+            shift_row<GS>(A);
+            g.sync();
+        }
+        if (status && r == 0) status[prob] = ok ? 0 : -1;
+        if (r < n) {
+            const double inv = 1.0 / diag.re;
+            const double xr = zr.re * inv, xi = zr.im * inv;
+            const int kr = ok ? level_index(xr, al) : 0;
+            const int ki = ok ? level_index(xi, al) : 0;
+            idx[2 * r] = (uint8_t)kr;
+            idx[2 * r + 1] = (uint8_t)ki;
+            xs[r] = {al.levels[kr], al.levels[ki]};
+        }
+    } else if (r < n) {
+        xs[r] = {al.levels[idx[2 * r]], al.levels[idx[2 * r + 1]]};
+    }
     g.sync();
 
     // residual r = y - H x_g and ||r||^2 (linear.py:44-47).  The sum of the
@@ -435,20 +388,18 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
             o.b[prob * N + n + r] = -c * im;
         }
         if (o.offset && r == 0) o.offset[prob] = r2 + 2.0 * tr;
-#if IL_PROBE_FRONT_RNG
-        // timing probe only: the x0 replay of the anneal kernel (32 anneals x
-        // 2n+1... here 65 draws each, 2 per lane-anneal chain) done here
-        // instead; written over G (wrong results)
-        {
-            constexpr int kS = 65;
-            for (int a = r; a < 32; a += GS) {
-                Pcg64 rng;
-                rng.seed_from(derive_seed2((uint64_t)prob * 977u, (uint64_t)a));
-                float* dst = reinterpret_cast<float*>(o.G + prob * (int64_t)N * N) + a * kS;
-                for (int i = 0; i < kS; ++i) dst[i] = (float)rng.uniform(-0.1, 0.2);
-            }
+        // lambda_max(G): the lanes read back the rows of c^2 A they wrote
+        // (B[r][j] = G[r][j] - i G[r][n + j]; the MMSE has eliminated A)
+#pragma unroll
+        for (int j = 0; j < GS; ++j)
+            A[j] = (r < n && j < n) ? cplx{Gr[j], -Gr[n + j]} : cplx{0.0, 0.0};
+        const double lam = lanczos_max_rows<GS>(g, A, n, vb, dsm, esm);
+        if (r == 0) {
+            const double S = (double)(2 * N + 1);
+            const double es = 32.0 / sqrt(fmax(lam, 1e-30) * S);
+            if (o.eps_scale) o.eps_scale[prob] = es;
+            if (o.eps_out) o.eps_out[prob] = o.fixed_eps > 0.0 ? o.fixed_eps : es * o.eps_gain;
         }
-#endif
     }
 }
 
@@ -461,13 +412,8 @@ int launch_rows_gs(const double* H, const double* y, const double* s2, int64_t P
     auto fn = k_front_rows<GS, M, I>;
     IL_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t blocks = (P + groups - 1) / groups;
-    cplx* scratch = nullptr;
-    if (M && I && IL_FRONT_SAVE_A)
-        if (const int rc = pool_alloc((void**)&scratch, sizeof(cplx) * GS * GS * (size_t)P, st)) return rc;
-    IL_LAUNCH(kProfFront, st, fn<<<(unsigned)blocks, kRowsThreads, smem, st>>>(H, y, s2, P, n_r, n, al, x_idx, energy, status, o, scratch););
-    const cudaError_t e = cudaGetLastError();
-    if (scratch) cudaFreeAsync(scratch, st);
-    IL_CHECK_CUDA(e);
+    IL_LAUNCH(kProfFront, st, fn<<<(unsigned)blocks, kRowsThreads, smem, st>>>(H, y, s2, P, n_r, n, al, x_idx, energy, status, o););
+    IL_CHECK_CUDA(cudaGetLastError());
     return IL_OK;
 }
 
