@@ -37,10 +37,6 @@ constexpr int kRowsThreads = 128;
 #define IL_GRAM_UNROLL 1
 #endif
 constexpr int kGramUnroll = IL_GRAM_UNROLL;
-#ifndef IL_ELIM_UNROLL  // unroll of the Gauss-Jordan step loop
-#define IL_ELIM_UNROLL 1
-#endif
-constexpr int kElimUnroll = IL_ELIM_UNROLL;
 
 // Per-group shared-memory slice (cplx units).
 IL_HD size_t rows_group_cplx(int n_r, int n, int GS) {
@@ -89,16 +85,6 @@ IL_D int exp2_of(double m) {  // m in [2^(e-1), 2^e) -> e (frexp exponent), m > 
     return (int)((__double_as_longlong(m) >> 52) & 0x7ff) - 1022;
 }
 IL_D double pow2(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
-
-// Drop column 0 of the lane's row: A[j] <- A[j + 1].  Keeping the active
-// column at index 0 lets the elimination loops stay rolled (small code, no
-// instruction-cache thrash) while every register index is static.
-template <int GS>
-IL_D void shift_row(cplx (&A)[GS]) {
-#pragma unroll
-    for (int j = 0; j + 1 < GS; ++j) A[j] = A[j + 1];
-    A[GS - 1] = {0.0, 0.0};
-}
 
 // Largest eigenvalue of a symmetric tridiagonal matrix (diagonal dd[0..m),
 // off-diagonal ee[0..m-1)), identical in every lane: Gershgorin bounds, an
@@ -312,29 +298,33 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
             if (j == r) A[j].re += s2;
         bool ok = true;
         cplx diag = {1.0, 0.0};
-        // Gauss-Jordan: pivot row k broadcast through vb (row) and misc (rhs);
-        // at step k, A[j] holds column k + j
-#pragma unroll kElimUnroll
-        for (int k = 0; k < n; ++k) {
-            if (r == k) {
+        // Gauss-Jordan, fully unrolled: at step k the pivot row's columns
+        // k..GS-1 are broadcast through vb (and its rhs through misc), and
+        // every other row eliminates column k, updating columns k+1.. only
+        // (static register indices, trimmed loops: half the FP64 work of a
+        // rolled loop over all columns)
 #pragma unroll
-                for (int j = 0; j < GS; ++j) vb[j] = A[j];
-                misc[0] = zr;
-            }
-            g.sync();
-            const double piv = vb[0].re;
-            ok = ok && (piv > 0.0);
-            const double inv = 1.0 / piv;
-            if (r == k) {
-                diag = A[0];
-            } else {
-                const cplx f = {A[0].re * inv, A[0].im * inv};
+        for (int k = 0; k < GS; ++k) {
+            if (k < n) {
+                if (r == k) {
 #pragma unroll
-                for (int j = 1; j < GS; ++j) A[j] = csub(A[j], cmul(f, vb[j]));
-                zr = csub(zr, cmul(f, misc[0]));
+                    for (int j = k; j < GS; ++j) vb[j] = A[j];
+                    misc[0] = zr;
+                }
+                g.sync();
+                const double piv = vb[k].re;
+                ok = ok && (piv > 0.0);
+                const double inv = 1.0 / piv;
+                if (r == k) {
+                    diag = A[k];
+                } else {
+                    const cplx f = {A[k].re * inv, A[k].im * inv};
+#pragma unroll
+                    for (int j = k + 1; j < GS; ++j) A[j] = csub(A[j], cmul(f, vb[j]));
+                    zr = csub(zr, cmul(f, misc[0]));
+                }
+                g.sync();
             }
-            shift_row<GS>(A);
-            g.sync();
         }
         if (status && r == 0) status[prob] = ok ? 0 : -1;
         if (r < n) {
