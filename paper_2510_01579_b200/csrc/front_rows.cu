@@ -148,9 +148,9 @@ IL_D double tridiag_max(double (&dd)[GS], double (&ee)[GS], int m) {
 // eigenvector is as unlikely as for a random one); n steps, or fewer when the
 // space becomes invariant (beta below 1e-14 of the row-sum norm; for B = c I
 // or B = 0 after one step).  No reorthogonalisation is needed for the
-// extreme Ritz value.  Measured against LAPACK eigvalsh on 2x10^4 16x16
-// Wishart matrices: 2.3e-15 relative (the Householder + Laguerre route this
-// replaces took 2.5x the FP64 work).  vb: 2*GS-cplx broadcast buffer of the
+// extreme Ritz value.  Emulated in numpy against LAPACK eigvalsh on 2x10^4
+// 16x16 Wishart matrices: 2.6e-15 relative worst case (the Householder +
+// Laguerre route this replaces took 2.5x the FP64 work).  vb: 2*GS-cplx broadcast buffer of the
 // group; dsm, esm: GS-double scratch.
 template <int GS>
 __device__ double lanczos_max_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx* vb,
@@ -186,10 +186,18 @@ __device__ double lanczos_max_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n
             w.re = fma(Bm[j].re, vj.re, fma(-Bm[j].im, vj.im, w.re));
             w.im = fma(Bm[j].re, vj.im, fma(Bm[j].im, vj.re, w.im));
         }
-        const double a = g.sum(v.re * w.re + v.im * w.im);
+        // alpha = v^H w and ||w||^2 in one reduction; then ||w'||^2 =
+        // ||w||^2 - alpha^2 - beta^2 for w' = w - alpha v - beta v_prev
+        // (exact for orthonormal v, v_prev), except where that difference
+        // cancels (< 1% of ||w||^2: about 1% of the steps on Wishart
+        // matrices, and every step of B = c I), which sums ||w'||^2 directly
+        double a = v.re * w.re + v.im * w.im, ww = cabs2(w);
+        g.sum2(a, ww);
         w = {w.re - a * v.re - beta * vp.re, w.im - a * v.im - beta * vp.im};
         if (r == 0) dsm[k] = a;
-        const double b = sqrt(g.sum(cabs2(w)));
+        double b2 = ww - a * a - beta * beta;
+        if (!(b2 >= 0.01 * ww)) b2 = g.sum(cabs2(w));
+        const double b = sqrt(b2);
         g.sync();  // vb is rewritten by the next step
         if (k == n - 1) break;
         if (!(b > 1e-14 * nrm)) {  // invariant subspace (or B = 0): T_{k+1} is exact
@@ -213,10 +221,10 @@ __device__ double lanczos_max_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n
 }
 
 template <int GS, bool DO_MMSE, bool DO_ISING>
-#ifndef IL_ROWS_MINB
-#define IL_ROWS_MINB 4
+#ifndef IL_ROWS_MINB  // CTAs per SM for GS = 16 (3: 168 registers, no spills; 4 spills)
+#define IL_ROWS_MINB 3
 #endif
-__global__ void __launch_bounds__(kRowsThreads, IL_ROWS_MINB)
+__global__ void __launch_bounds__(kRowsThreads, GS == 16 ? IL_ROWS_MINB : 4)
 k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
              const double* __restrict__ s2g, int64_t P, int n_r, int n, Alphabet al,
              uint8_t* __restrict__ x_idx, double* __restrict__ energy,

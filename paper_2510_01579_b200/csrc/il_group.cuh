@@ -21,6 +21,15 @@ struct Grp {
         for (int o = GS / 2; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(mask, v, o, GS));
         return v;
     }
+    // two sums with their shuffle trees interleaved (one tree's latency)
+    __device__ void sum2(double& a, double& b) const {
+#pragma unroll
+        for (int o = GS / 2; o > 0; o >>= 1) {
+            const double ta = __shfl_xor_sync(mask, a, o, GS), tb = __shfl_xor_sync(mask, b, o, GS);
+            a = __dadd_rn(a, ta);
+            b = __dadd_rn(b, tb);
+        }
+    }
     __device__ double bcast(double v, int src) const { return __shfl_sync(mask, v, src, GS); }
     __device__ cplx bcast(cplx v, int src) const { return {bcast(v.re, src), bcast(v.im, src)}; }
     __device__ void sync() const { __syncwarp(mask); }
