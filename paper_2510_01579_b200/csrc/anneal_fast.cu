@@ -67,6 +67,9 @@ constexpr int kWarpsPerCta = IL_FAST_WARPS;
 #define IL_STEP_UNROLL 2
 #endif
 constexpr int kStepUnroll = IL_STEP_UNROLL;
+#ifndef IL_REFRESH_PASSES  // A/B: 3 = hi*hi + lo_v*hi_G + hi_v*lo_G; 20 = drop lo_v; 21 = drop lo_G
+#define IL_REFRESH_PASSES 3
+#endif
 
 
 template <int NT>
@@ -304,20 +307,27 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
             for (int kt = 0; kt < KT; ++kt) {
                 // A fragment: a0 = (g, 2t..), a1 = (g+8, 2t..), a2 = (g, 2t+8..), a3 = (g+8, 2t+8..)
                 uint32_t ahi[4], alo[4];
-                split_h2(v[0][2 * kt], ahi[0], alo[0]);
-                split_h2(v[1][2 * kt], ahi[1], alo[1]);
-                if (2 * kt + 1 < NT) {
-                    split_h2(v[0][2 * kt + 1], ahi[2], alo[2]);
-                    split_h2(v[1][2 * kt + 1], ahi[3], alo[3]);
+                if (SPLIT && IL_REFRESH_PASSES != 20) {
+                    split_h2(v[0][2 * kt], ahi[0], alo[0]);
+                    split_h2(v[1][2 * kt], ahi[1], alo[1]);
+                    if (2 * kt + 1 < NT) {
+                        split_h2(v[0][2 * kt + 1], ahi[2], alo[2]);
+                        split_h2(v[1][2 * kt + 1], ahi[3], alo[3]);
+                    } else {
+                        ahi[2] = ahi[3] = alo[2] = alo[3] = 0u;
+                    }
                 } else {
-                    ahi[2] = ahi[3] = alo[2] = alo[3] = 0u;
+                    ahi[0] = h2_bits(__float22half2_rn(v[0][2 * kt]));
+                    ahi[1] = h2_bits(__float22half2_rn(v[1][2 * kt]));
+                    ahi[2] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(v[0][2 * kt + 1])) : 0u;
+                    ahi[3] = 2 * kt + 1 < NT ? h2_bits(__float22half2_rn(v[1][2 * kt + 1])) : 0u;
                 }
 #pragma unroll
                 for (int n = 0; n < NT; ++n) {
                     const uint4 f = frag[(kt * NT + n) * 32 + lane];
                     if (SPLIT) {
-                        mma_f16(acc[n], alo, f.x, f.y);
-                        mma_f16(acc[n], ahi, f.z, f.w);
+                        if (IL_REFRESH_PASSES != 20) mma_f16(acc[n], alo, f.x, f.y);
+                        if (IL_REFRESH_PASSES != 21) mma_f16(acc[n], ahi, f.z, f.w);
                     }
                     mma_f16(acc[n], ahi, f.x, f.y);
                 }
