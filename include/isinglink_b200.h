@@ -41,8 +41,11 @@ enum il_precision {
     IL_PREC_FP32 = 1,       /* FP32 state, coupling product on tensor cores as a
                                3-pass f16 hi/lo split (hi*hi + lo*hi + hi*lo, FP32
                                accumulate; FP32-accurate); the throughput mode */
-    IL_PREC_TF32 = 2        /* FP32 state, single-pass f16 coupling product
+    IL_PREC_TF32 = 2,       /* FP32 state, single-pass f16 coupling product
                                (11-bit significand, like TF32) */
+    IL_PREC_MIXED = 3       /* FP32 state; coupling product as IL_PREC_FP32 for the
+                               first 16 steps, then 2 passes (hi*hi + hi*lo: G split
+                               to FP32 accuracy, the state rounded to f16) */
 };
 
 /* Solver configuration — mirrors CacParams (solver.py:87-124). */

@@ -16,7 +16,7 @@ LIB_PATH = os.environ.get(
     os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libisinglink_b200.so"))
 
 IL_OK, IL_ERR_ARG, IL_ERR_CUDA, IL_ERR_UNSUPPORTED, IL_ERR_NOMEM = 0, -1, -2, -3, -4
-PREC = {"fp64_exact": 0, "fp32": 1, "tf32": 2}
+PREC = {"fp64_exact": 0, "fp32": 1, "tf32": 2, "mixed": 3}
 
 _c_d = ctypes.c_double
 _c_i32 = ctypes.c_int32

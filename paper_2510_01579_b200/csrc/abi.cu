@@ -153,7 +153,7 @@ static int validate(const il_cac_params* p) {
     const double floor_ = sqrt(fmax(fmax(p->a, p->p - 1.0), 0.0));
     IL_REQUIRE(p->diverge_threshold > floor_,
                "diverge_threshold must exceed sqrt(max(a, p - 1)) = %.3g", floor_);
-    IL_REQUIRE(p->precision >= IL_PREC_FP64_EXACT && p->precision <= IL_PREC_TF32,
+    IL_REQUIRE(p->precision >= IL_PREC_FP64_EXACT && p->precision <= IL_PREC_MIXED,
                "unknown precision %d", p->precision);
     return IL_OK;
 }

@@ -40,7 +40,7 @@ constexpr int kGramUnroll = IL_GRAM_UNROLL;
 
 // Per-group shared-memory slice (cplx units).
 IL_HD size_t rows_group_cplx(int n_r, int n, int GS) {
-    return (size_t)n_r * n + 2 * (size_t)n_r + 6 * (size_t)GS + 2 + 1;
+    return (size_t)n_r * n + 2 * (size_t)n_r + 6 * (size_t)GS + 3 + 1;
 }
 
 // A row r = sum_k conj(H[k][r]) H[k][:] (zero rows/cols beyond n), z_r = (H^H y)_r.
@@ -142,19 +142,20 @@ IL_D double tridiag_max(double (&dd)[GS], double (&ee)[GS], int m) {
     return x * pow2(ex);
 }
 
-// Largest eigenvalue of the Hermitian matrix whose row r lives in lane r's
-// B (kept).  Lanczos: T_k = V^H B V over the Krylov space of a fixed start
+// Lanczos tridiagonalisation of the Hermitian matrix whose row r lives in
+// lane r's B (kept): T_k = V^H B V over the Krylov space of a fixed start
 // vector with irregular entries (a start vector orthogonal to the top
 // eigenvector is as unlikely as for a random one); n steps, or fewer when the
 // space becomes invariant (beta below 1e-14 of the row-sum norm; for B = c I
 // or B = 0 after one step).  No reorthogonalisation is needed for the
 // extreme Ritz value.  Emulated in numpy against LAPACK eigvalsh on 2x10^4
 // 16x16 Wishart matrices: 2.6e-15 relative worst case (the Householder +
-// Laguerre route this replaces took 2.5x the FP64 work).  vb: 2*GS-cplx broadcast buffer of the
-// group; dsm, esm: GS-double scratch.
+// Laguerre route this replaces took 2.5x the FP64 work).  vb: 2*GS-cplx
+// broadcast buffer of the group; T goes to dsm (diagonal) and esm
+// (sub-diagonal); returns its order m.
 template <int GS>
-__device__ double lanczos_max_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx* vb,
-                                   double* dsm, double* esm) {
+__device__ int lanczos_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx* vb,
+                            double* dsm, double* esm) {
     const int r = g.r;
     // start vector: (0.5 + frac((r+1) phi)) + i (0.5 + frac(3.1 (r+1) phi^2)), normalised
     cplx v = {0.0, 0.0};
@@ -210,39 +211,27 @@ __device__ double lanczos_max_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n
         v = {w.re * ib, w.im * ib};
         beta = b;
     }
-    g.sync();
-    double dd[GS], ee[GS];
-#pragma unroll
-    for (int k = 0; k < GS; ++k) {
-        dd[k] = k < m ? dsm[k] : 0.0;
-        ee[k] = k + 1 < m ? esm[k] : 0.0;
-    }
-    return tridiag_max<GS>(dd, ee, m);
+    return m;
 }
 
+// Per-group slice: ... misc[2] holds the order m of the Lanczos tridiagonal
+// T (d in dsm, e in esm) for the CTA's eigenvalue stage.
 template <int GS, bool DO_MMSE, bool DO_ISING>
-#ifndef IL_ROWS_MINB  // CTAs per SM for GS = 16 (3: 168 registers, no spills; 4 spills)
-#define IL_ROWS_MINB 3
-#endif
-__global__ void __launch_bounds__(kRowsThreads, GS == 16 ? IL_ROWS_MINB : 4)
-k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
-             const double* __restrict__ s2g, int64_t P, int n_r, int n, Alphabet al,
-             uint8_t* __restrict__ x_idx, double* __restrict__ energy,
-             int8_t* __restrict__ status, IsingOut o) {
-    extern __shared__ __align__(16) cplx smem_c[];
-    const Grp<GS> g;
+__device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx* H,
+                                            const double* __restrict__ Hg,
+                                            const double* __restrict__ yg,
+                                            const double* __restrict__ s2g, int n_r, int n,
+                                            const Alphabet& al, uint8_t* __restrict__ x_idx,
+                                            double* __restrict__ energy,
+                                            int8_t* __restrict__ status, const IsingOut& o) {
     const int r = g.r;
-    const int grp = threadIdx.x / GS;
-    const int64_t prob = (int64_t)blockIdx.x * (kRowsThreads / GS) + grp;
-    if (prob >= P) return;  // whole groups exit together
-    cplx* H = smem_c + grp * rows_group_cplx(n_r, n, GS);
     cplx* y = H + n_r * n;
     cplx* res = y + n_r;
     cplx* vb = res + n_r;
     cplx* wb = vb + 2 * GS;
     cplx* xs = wb + 2 * GS;    // decided symbols x_g (GS)
-    cplx* misc = xs + GS;      // [0] = Gauss-Jordan rhs broadcast
-    double* dsm = reinterpret_cast<double*>(misc + 2);  // tridiagonal d[GS]
+    cplx* misc = xs + GS;      // [0] = Gauss-Jordan rhs broadcast, [2].re = order of T
+    double* dsm = reinterpret_cast<double*>(misc + 3);  // tridiagonal d[GS]
     double* esm = dsm + GS;                              // and e[GS]
     uint8_t* idx = x_idx + prob * 2 * n;
     {
@@ -298,6 +287,11 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
             tr = 2.0 * gi;
         }
         tr = g.sum(tr);
+        // lambda_max(G) = c^2 lambda_max(A): Lanczos on the register rows of A
+        // while they are intact (the MMSE below eliminates them in place); the
+        // eigenvalue of T is taken by the CTA's last stage
+        const int m = lanczos_rows<GS>(g, A, n, vb, dsm, esm);
+        if (r == 0) misc[2].re = (double)m;
     }
     if (DO_MMSE) {
         const double s2 = s2g[prob];
@@ -386,19 +380,52 @@ k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
             o.b[prob * N + n + r] = -c * im;
         }
         if (o.offset && r == 0) o.offset[prob] = r2 + 2.0 * tr;
-        // lambda_max(G): the lanes read back the rows of c^2 A they wrote
-        // (B[r][j] = G[r][j] - i G[r][n + j]; the MMSE has eliminated A)
-#pragma unroll
-        for (int j = 0; j < GS; ++j)
-            A[j] = (r < n && j < n) ? cplx{Gr[j], -Gr[n + j]} : cplx{0.0, 0.0};
-        const double lam = lanczos_max_rows<GS>(g, A, n, vb, dsm, esm);
-        if (r == 0) {
-            const double S = (double)(2 * N + 1);
-            const double es = 32.0 / sqrt(fmax(lam, 1e-30) * S);
-            if (o.eps_scale) o.eps_scale[prob] = es;
-            if (o.eps_out) o.eps_out[prob] = o.fixed_eps > 0.0 ? o.fixed_eps : es * o.eps_gain;
-        }
     }
+}
+
+template <int GS, bool DO_MMSE, bool DO_ISING>
+#ifndef IL_ROWS_MINB  // CTAs per SM for GS = 16 (3: 168 registers, no spills; 4 spills)
+#define IL_ROWS_MINB 3
+#endif
+__global__ void __launch_bounds__(kRowsThreads, GS == 16 ? IL_ROWS_MINB : 4)
+k_front_rows(const double* __restrict__ Hg, const double* __restrict__ yg,
+             const double* __restrict__ s2g, int64_t P, int n_r, int n, Alphabet al,
+             uint8_t* __restrict__ x_idx, double* __restrict__ energy,
+             int8_t* __restrict__ status, IsingOut o) {
+    extern __shared__ __align__(16) cplx smem_c[];
+    constexpr int kGroups = kRowsThreads / GS;
+    const size_t slice = rows_group_cplx(n_r, n, GS);
+    {
+        const Grp<GS> g;
+        const int grp = threadIdx.x / GS;
+        const int64_t prob = (int64_t)blockIdx.x * kGroups + grp;
+        if (prob < P)  // whole groups together
+            front_group<GS, DO_MMSE, DO_ISING>(g, prob, smem_c + grp * slice, Hg, yg, s2g, n_r, n, al,
+                                               x_idx, energy, status, o);
+    }
+    if (!DO_ISING) return;
+    // eigenvalue stage: lambda_max of each group's Lanczos tridiagonal, one
+    // thread per resource element (the Laguerre iteration is sequential; run
+    // once instead of redundantly in every lane of the group)
+    __syncthreads();
+    const int64_t prob = (int64_t)blockIdx.x * kGroups + threadIdx.x;
+    if (threadIdx.x >= kGroups || prob >= P) return;
+    const cplx* misc = smem_c + threadIdx.x * slice + (size_t)n_r * n + 2 * (size_t)n_r + 5 * GS;
+    const double* dsm = reinterpret_cast<const double*>(misc + 3);
+    const double* esm = dsm + GS;
+    const int m = (int)misc[2].re;
+    double dd[GS], ee[GS];
+#pragma unroll
+    for (int k = 0; k < GS; ++k) {
+        dd[k] = k < m ? dsm[k] : 0.0;
+        ee[k] = k + 1 < m ? esm[k] : 0.0;
+    }
+    const double c = 0.5 * al.spacing;
+    const double lam = (c * c) * tridiag_max<GS>(dd, ee, m);
+    const double S = (double)(4 * n + 1);
+    const double es = 32.0 / sqrt(fmax(lam, 1e-30) * S);
+    if (o.eps_scale) o.eps_scale[prob] = es;
+    if (o.eps_out) o.eps_out[prob] = o.fixed_eps > 0.0 ? o.fixed_eps : es * o.eps_gain;
 }
 
 template <int GS, bool M, bool I>

@@ -8,7 +8,10 @@ the B200 arithmetic mode.
     3-pass f16 hi/lo split (hi*hi + lo*hi + hi*lo, FP32 accumulate;
     FP32-accurate); the throughput mode;
   * ``"tf32"`` — single-pass f16 coupling product (11-bit significand, like
-    TF32; fastest, least accurate).
+    TF32; fastest, least accurate);
+  * ``"mixed"`` — ``"fp32"`` for the first 16 steps, then a 2-pass product
+    (G split to FP32 accuracy, the state rounded to f16): the early steps,
+    where the chaotic dynamics amplify rounding, keep FP32 accuracy.
 
 Reference ``CacParams`` objects (no ``precision`` attribute) are accepted
 everywhere and run in ``DEFAULT_PRECISION``.

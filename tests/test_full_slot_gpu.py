@@ -60,6 +60,19 @@ def test_headline_slot_16x16_16qam_20db():
     assert same >= 0.99
 
 
+def test_headline_slot_mixed_mode():
+    """The "mixed" precision mode (coupling product's third split pass
+    dropped after 16 steps) on the headline slot: same >= 99% energy gate."""
+    import bench
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    H, y, nv, seeds, truth = bench.headline_slot(torch.device("cuda", torch.cuda.current_device()))
+    ex = batched.detect_cim_batch(H, y, nv, 16, seeds, CacParams(precision="fp64_exact"))
+    fa = batched.detect_cim_batch(H, y, nv, 16, seeds, CacParams(precision="mixed"))
+    _, same = _compare("16x16 16-QAM 20 dB (headline), mixed", fa, ex, truth)
+    assert same >= 0.99
+
+
 @pytest.mark.parametrize("n_t,order,snr", [(8, 16, 20.0), (16, 64, 25.0)])
 def test_full_slot_uplink(n_t, order, snr):
     import bench

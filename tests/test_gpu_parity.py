@@ -126,7 +126,7 @@ def test_detect_cim_exact_matches_reference(name):
     assert np.array_equal(r.diverged.cpu().numpy(), d["diverged"])
 
 
-@pytest.mark.parametrize("precision", ["fp32", "tf32"])
+@pytest.mark.parametrize("precision", ["fp32", "mixed", "tf32"])
 @pytest.mark.parametrize("name", DET_SETS)
 def test_detect_cim_fast_energy_parity(name, precision):
     """Throughput mode: final energy <= reference on >= 99% of instances."""
@@ -140,7 +140,7 @@ def test_detect_cim_fast_energy_parity(name, precision):
     frac = ok.mean()
     print(f"{name} {precision}: energy<=ref {frac:.4f}, identical decisions "
           f"{np.all(r.x_idx.cpu().numpy() == d['x_hat'], axis=(1, 2)).mean():.4f}")
-    assert frac >= (0.99 if precision == "fp32" else 0.97)
+    assert frac >= (0.97 if precision == "tf32" else 0.99)
 
 
 def test_precode_vpp_matches_reference():

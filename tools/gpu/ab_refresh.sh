@@ -1,7 +1,7 @@
 # A/B of refresh-pass variants: slot time + parity against fp64_exact at scale
 cd $GRAFT_REPO_ROOT
-./tools/microbench/mma_kinds
-for v in default "$@"; do
+[ "$MB" = 1 ] && ./tools/microbench/mma_kinds
+for v in ${VARIANTS:-default} "$@"; do
   echo "== $v"
   if [ "$v" = default ]; then L=paper_2510_01579_b200/_lib/libisinglink_b200.so; else L=build/var/$v/libisinglink_b200.so; fi
   ISINGLINK_B200_LIB=$L python tools/quick_bench.py 16 16 45864 fp32 5 2>&1 | grep -v Warn | tail -1
