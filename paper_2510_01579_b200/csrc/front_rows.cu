@@ -178,15 +178,23 @@ __device__ int lanczos_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx*
     int m = n;
 #pragma unroll 1
     for (int k = 0; k < n; ++k) {
-        vb[r] = v;
+        // v_k is broadcast through one of two halves of vb, alternating, so
+        // that one group barrier per step separates writes from reads
+        cplx* vk = vb + (k & 1) * GS;
+        vk[r] = v;
         g.sync();
-        cplx w = {0.0, 0.0};
+        // w = B v with the even and odd columns in separate accumulators
+        // (half the dependent-FMA chain)
+        cplx w0 = {0.0, 0.0}, w1 = {0.0, 0.0};
 #pragma unroll
-        for (int j = 0; j < GS; ++j) {
-            const cplx vj = vb[j];
-            w.re = fma(Bm[j].re, vj.re, fma(-Bm[j].im, vj.im, w.re));
-            w.im = fma(Bm[j].re, vj.im, fma(Bm[j].im, vj.re, w.im));
+        for (int j = 0; j < GS; j += 2) {
+            const cplx v0 = vk[j], v1 = vk[j + 1];
+            w0.re = fma(Bm[j].re, v0.re, fma(-Bm[j].im, v0.im, w0.re));
+            w0.im = fma(Bm[j].re, v0.im, fma(Bm[j].im, v0.re, w0.im));
+            w1.re = fma(Bm[j + 1].re, v1.re, fma(-Bm[j + 1].im, v1.im, w1.re));
+            w1.im = fma(Bm[j + 1].re, v1.im, fma(Bm[j + 1].im, v1.re, w1.im));
         }
+        cplx w = {w0.re + w1.re, w0.im + w1.im};
         // alpha = v^H w and ||w||^2 in one reduction; then ||w'||^2 =
         // ||w||^2 - alpha^2 - beta^2 for w' = w - alpha v - beta v_prev
         // (exact for orthonormal v, v_prev), except where that difference
@@ -199,7 +207,6 @@ __device__ int lanczos_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx*
         double b2 = ww - a * a - beta * beta;
         if (!(b2 >= 0.01 * ww)) b2 = g.sum(cabs2(w));
         const double b = sqrt(b2);
-        g.sync();  // vb is rewritten by the next step
         if (k == n - 1) break;
         if (!(b > 1e-14 * nrm)) {  // invariant subspace (or B = 0): T_{k+1} is exact
             m = k + 1;
@@ -211,6 +218,7 @@ __device__ int lanczos_rows(const Grp<GS>& g, const cplx (&Bm)[GS], int n, cplx*
         v = {w.re * ib, w.im * ib};
         beta = b;
     }
+    g.sync();  // the last v_k has been read before vb is reused
     return m;
 }
 
@@ -239,7 +247,6 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
         const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
         for (int i = r; i < n_r * n; i += GS) H[i] = Hp[i];
         for (int i = r; i < n_r; i += GS) y[i] = yp[i];
-        vb[GS + r] = wb[GS + r] = cplx{0.0, 0.0};  // zero tails read by shifted columns
     }
     g.sync();
     const double c = 0.5 * al.spacing;
@@ -305,16 +312,19 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
         // every other row eliminates column k, updating columns k+1.. only
         // (static register indices, trimmed loops: half the FP64 work of a
         // rolled loop over all columns)
+        // (pivot rows alternate between the two halves of vb, their rhs
+        // between misc[0] and misc[1]: one group barrier per step)
 #pragma unroll
         for (int k = 0; k < GS; ++k) {
             if (k < n) {
+                cplx* pk = vb + (k & 1) * GS;
                 if (r == k) {
 #pragma unroll
-                    for (int j = k; j < GS; ++j) vb[j] = A[j];
-                    misc[0] = zr;
+                    for (int j = k; j < GS; ++j) pk[j] = A[j];
+                    misc[k & 1] = zr;
                 }
                 g.sync();
-                const double piv = vb[k].re;
+                const double piv = pk[k].re;
                 ok = ok && (piv > 0.0);
                 const double inv = 1.0 / piv;
                 if (r == k) {
@@ -322,10 +332,9 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
                 } else {
                     const cplx f = {A[k].re * inv, A[k].im * inv};
 #pragma unroll
-                    for (int j = k + 1; j < GS; ++j) A[j] = csub(A[j], cmul(f, vb[j]));
-                    zr = csub(zr, cmul(f, misc[0]));
+                    for (int j = k + 1; j < GS; ++j) A[j] = csub(A[j], cmul(f, pk[j]));
+                    zr = csub(zr, cmul(f, misc[k & 1]));
                 }
-                g.sync();
             }
         }
         if (status && r == 0) status[prob] = ok ? 0 : -1;
