@@ -36,6 +36,7 @@ struct FastScalars {
     int b_valid;  // anneal rows per problem that enter the selection (screened energies)
     int b_out;    // anneal rows per problem whose steps / mvms are counted (PAD + counts)
     int full_steps;  // refreshes at steps < full_steps take the lo(v) x hi(G) pass too
+    int64_t n_probs; // problems in the launch (PACK: the last warp may hold one)
 };
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }

@@ -1,5 +1,6 @@
 // Internal launch interfaces shared by the .cu translation units.
 #pragma once
+#include <cstdlib>
 #include "il_common.cuh"
 
 namespace il {
@@ -49,7 +50,16 @@ int launch_anneal_umma(const double* G, const double* g, const double* b,
                        const void* fast_scalars, bool split, bool same_qr, int8_t* spins,
                        uint8_t* diverged, double* energies, bool screened, cudaStream_t st);
 // anneal rows per problem the fast kernel runs for B requested anneals
-inline int fast_rows(int B) { return (B + 15) / 16 * 16; }
+// Anneal rows per problem in the fast kernel: 8 (two problems per warp) for
+// n_anneals <= 8, else tiles of 16; the extra rows are seeded by their own
+// index and never selected.
+// ISINGLINK_PACK=0 (read per call) keeps n_anneals <= 8 in padded 16-row
+// tiles: the parity test compares both layouts bit for bit.
+inline int fast_rows(int B) {
+    const char* e = getenv("ISINGLINK_PACK");
+    const bool pack = !(e && *e == '0');
+    return (B <= 8 && pack) ? 8 : (B + 15) / 16 * 16;
+}
 
 // ---- front-end / reduction kernels -----------------------------------------
 // Ising outputs of the front-end kernels (any pointer may be null).
