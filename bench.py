@@ -193,9 +193,10 @@ def run_reference(args) -> None:
     import multiprocessing as mp
     cores = host_cores()
     kind = cpu_kind()
-    # ~128 REs per process per step (about 2 s of CPU work per step at the
-    # measured ~8 k det/s on 16 cores): pool dispatch overhead stays small
-    per_step = cores * 128
+    # 1024 REs per process per step: about 2 s of CPU work per step at the
+    # measured ~8 k det/s on 16 cores, so pool dispatch and the fork warm-up
+    # stay small against it (a 25-step driver run takes under a minute)
+    per_step = cores * 1024
     pool = mp.get_context("fork").Pool(cores, initializer=_cpu_init)
     pool.map(_cpu_worker, cpu_instances(cores), chunksize=1)
     for _ in range(args.warmup):
@@ -388,7 +389,7 @@ def stage_rooflines(prof, steps, P, n_anneals) -> dict:
     for kind, nbytes in stage_bytes(N_R, N_T, n_anneals).items():
         ms = prof.get(kind, (0.0, 0))[0] / max(steps, 1)
         gbs = nbytes * P / (ms * 1e-3) / 1e9 if ms > 0 else None
-        bound = ("latency (FP64 elimination / Householder chains)" if kind == "front"
+        bound = ("latency (FP64 Gauss-Jordan / Lanczos chains)" if kind == "front"
                  else "HBM + latency (TMA-staged H, y; int8 spins)")
         out[kind] = {"bound": bound, "bytes_per_re": nbytes,
                      "achieved": gbs, "peak": peak, "unit": "GB/s",

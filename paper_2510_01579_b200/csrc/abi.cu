@@ -182,7 +182,7 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
                              const double* offset, const double* eps, const uint64_t* base,
                              const il_cac_params* prm, uint8_t* x_idx, double* energy,
                              int8_t* source, int32_t* anneal_index, int32_t* diverged_count,
-                             cudaStream_t st) {
+                             cudaStream_t st, const double* gstats = nullptr) {
     Workspace ws(st);  // per stage: released (stream-ordered) when the stage is enqueued
     const int N = 2 * n_t, S = 2 * N + 1, B = prm->n_anneals;
     const AnnealScalars s = scalars_of(prm);
@@ -203,7 +203,7 @@ static int anneal_and_select(const double* H, const double* y, int64_t P, int n_
         energies = ws.get<double>((size_t)P * Bs, &rc);
         if (rc) return rc;
         rc = launch_anneal_fast(G, g, b, base, eps, P, N, Bs, s, prm->precision, spins, div,
-                                energies, st, /*screen_rows=*/B);
+                                energies, st, /*screen_rows=*/B, nullptr, nullptr, 0, gstats);
     } else {
         rc = launch_anneal_exact(G, g, b, nullptr, base, eps, P, N, B, s, spins, div, nullptr,
                                  nullptr, st);
@@ -365,15 +365,18 @@ int il_detect_cim_batch(const double* H, const double* y, const double* noise_va
     uint64_t* base = ws.get<uint64_t>((size_t)P, &rc);
     double* en = energy ? energy : ws.get<double>((size_t)P, &rc);
     int8_t* src = source ? source : ws.get<int8_t>((size_t)P, &rc);
+    // the row front end also hands the anneal its operand scale and screen
+    // bound (max |G|, sum |G| + sum |b|) so that it need not scan G again
+    double* gstats = front_rows_supported(n_r, n_t) ? ws.get<double>((size_t)P * 2, &rc) : nullptr;
     if (rc) return rc;
     const double fixed = prm->eps > 0.0 ? prm->eps : 0.0;
     rc = launch_mmse_ising(H, y, noise_var, P, n_r, n_t, al, x_idx, en, src, G, g, b, off, eps, 1.0,
-                           fixed, st);
+                           fixed, st, gstats);
     if (rc) return rc;
     rc = launch_base_seeds(seed, P, 0, 0, base, st);  // detector.py:67 derive_seed(seed, 0, 0)
     if (rc) return rc;
     return anneal_and_select(H, y, P, n_r, n_t, al, G, g, b, off, eps, base, prm, x_idx, en, src,
-                             anneal_index, diverged_count, st);
+                             anneal_index, diverged_count, st, gstats);
 }
 
 int il_residual_batch(const double* H, const double* y, const double* x, int64_t P, int32_t n_r,

@@ -72,7 +72,7 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
                        double* energies, cudaStream_t st, int screen_rows, int64_t* steps,
-                       int64_t* mvms, int count_rows) {
+                       int64_t* mvms, int count_rows, const double* gstats) {
     if (!fast_anneal_supported(N, B, s)) {
         set_error("fast anneal kernel does not support n_dim=%d n_anneals=%d with these params", N, B);
         return IL_ERR_UNSUPPORTED;
@@ -96,6 +96,7 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.b_out = count_rows;
     fs.full_steps = full_steps_for(s.n_steps, precision);
     fs.n_probs = P;
+    fs.gstats = gstats;
     IL_REQUIRE((steps == nullptr) == (mvms == nullptr) && (!steps || (count_rows > 0 && count_rows <= B)),
                "fast anneal: steps and mvms go together, for 1..B rows");
     // the screen pays off from N = 24 on (at N = 16 the FP64 epilogue is cheaper)

@@ -206,7 +206,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         const double K = s.dt * eps_p[probh[q]];
         const double* Gp = Gq[q];
         double gmax = 0.0;
-        if (screened) {
+        if (s.gstats) {
+            // precomputed by the front end (k_front_rows) while it held the rows
+            gmax = s.gstats[2 * probh[q]];
+            if (screened && lane == 0)
+                reinterpret_cast<double*>(frag + L::kKgF4 - 1)[q] = s.gstats[2 * probh[q] + 1];
+        } else if (screened) {
             double mag = 0.0;  // sum |G| + sum |b|: the screen bound, parked in shared memory
 #pragma unroll 4
             for (int i = lane; i < nr * nr; i += 32) {

@@ -772,9 +772,12 @@ int launch_build_ising(const double* H, const double* y, const uint8_t* guess_id
 int launch_mmse_ising(const double* H, const double* y, const double* noise_var, int64_t P,
                       int n_r, int n_t, const Alphabet& al, uint8_t* x_idx, double* energy,
                       int8_t* status, double* G, double* g_diag, double* b, double* offset,
-                      double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st) {
+                      double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st,
+                      double* gstats) {
     if (P == 0) return IL_OK;
     IsingOut o{G, g_diag, b, offset, nullptr, eps_out, eps_gain, fixed_eps};
+    IL_REQUIRE(!gstats || front_rows_supported(n_r, n_t), "gstats come from the row front end only");
+    o.gstats = gstats;
     if (front_rows_supported(n_r, n_t))
         return launch_front_rows(true, true, H, y, noise_var, P, n_r, n_t, al, x_idx, energy,
                                  status, o, st);

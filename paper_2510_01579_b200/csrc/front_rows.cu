@@ -256,6 +256,7 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
     cplx zr;
     gram_row<GS>(H, y, n_r, n, r, A, &zr);
     double tr = 0.0;
+    double gmax = 0.0, gsum = 0.0;  // max |G| and sum |G| over rows r, n + r (o.gstats)
     double* Gr = o.G + prob * (int64_t)N * N + (int64_t)r * N;  // G row r (valid for r < n)
     if (DO_ISING) {
         // G rows r and n + r (16-byte stores), g_diag, trace
@@ -281,6 +282,18 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
                         }
                     }
                 }
+            }
+            if (o.gstats) {
+                // the stored magnitudes: |c2 Re A|, |c2 Im A|, twice each
+#pragma unroll
+                for (int j = 0; j < GS; ++j) {
+                    if (j < n) {
+                        const double ar = fabs(c2 * A[j].re), ai = fabs(c2 * A[j].im);
+                        gmax = fmax(gmax, fmax(ar, ai));
+                        gsum += ar + ai;
+                    }
+                }
+                gsum *= 2.0;
             }
             double arr = 0.0;
 #pragma unroll
@@ -387,8 +400,19 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
             }
             o.b[prob * N + r] = -c * re;
             o.b[prob * N + n + r] = -c * im;
+            gsum += fabs(-c * re) + fabs(-c * im);
         }
         if (o.offset && r == 0) o.offset[prob] = r2 + 2.0 * tr;
+        if (o.gstats) {
+            // the anneal's operand scale and screen bound (k_anneal_fast)
+#pragma unroll
+            for (int q = GS / 2; q > 0; q >>= 1) gmax = fmax(gmax, __shfl_xor_sync(g.mask, gmax, q, GS));
+            gsum = g.sum(gsum);
+            if (r == 0) {
+                o.gstats[2 * prob] = gmax;
+                o.gstats[2 * prob + 1] = gsum;
+            }
+        }
     }
 }
 

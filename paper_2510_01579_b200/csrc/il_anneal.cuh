@@ -37,6 +37,7 @@ struct FastScalars {
     int b_out;    // anneal rows per problem whose steps / mvms are counted (PAD + counts)
     int full_steps;  // refreshes at steps < full_steps take the lo(v) x hi(G) pass too
     int64_t n_probs; // problems in the launch (PACK: the last warp may hold one)
+    const double* gstats;  // [P][2] max |G|, sum |G| + sum |b| from the front end, or null
 };
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }

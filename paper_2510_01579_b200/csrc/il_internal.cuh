@@ -36,7 +36,8 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
                        const uint64_t* base_seed, const double* eps_p, int64_t P, int N, int B,
                        const AnnealScalars& s, int precision, int8_t* spins, uint8_t* diverged,
                        double* energies, cudaStream_t st, int screen_rows = 0,
-                       int64_t* steps = nullptr, int64_t* mvms = nullptr, int count_rows = 0);
+                       int64_t* steps = nullptr, int64_t* mvms = nullptr, int count_rows = 0,
+                       const double* gstats = nullptr);
 bool fast_anneal_supported(int N, int B, const AnnealScalars& s);
 // launch_anneal_fast hands the shape to the tcgen05 kernel (opt-in)
 bool fast_anneal_uses_umma(int N, int B);
@@ -66,6 +67,9 @@ inline int fast_rows(int B) {
 struct IsingOut {
     double *G, *g, *b, *offset, *eps_scale, *eps_out;
     double eps_gain, fixed_eps;
+    // optional [P][2]: max |G| and sum |G| + sum |b| (k_front_rows only), read
+    // by the fast anneal instead of scanning G
+    double* gstats = nullptr;
 };
 // Register-resident front-end for n_t <= 16 (front_rows.cu).
 bool front_rows_supported(int n_r, int n_t);
@@ -104,7 +108,8 @@ int launch_select_decode(const double* H, const double* y, const double* G, cons
 int launch_mmse_ising(const double* H, const double* y, const double* noise_var, int64_t P,
                       int n_r, int n_t, const Alphabet& al, uint8_t* x_idx, double* energy,
                       int8_t* status, double* G, double* g_diag, double* b, double* offset,
-                      double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st);
+                      double* eps_out, double eps_gain, double fixed_eps, cudaStream_t st,
+                      double* gstats = nullptr);
 // MMGaP-E (multi.cu)
 int launch_mmse_sic(const double* H, const double* y, const double* noise_var, int64_t P, int n_r,
                     int n_t, const Alphabet& al, uint8_t* x_idx, double* energy, int8_t* status,
