@@ -334,7 +334,13 @@ def other_configs(dev, prm) -> dict:
         "ser": (rm.x_idx != truthh).any(-1).float().mean().item(),
         "energy_le_exact": (rm.energy <= r.energy * (1 + 1e-12)).float().mean().item(),
         "identical_decisions": (rm.x_idx == r.x_idx).all(-1).all(-1).float().mean().item()}
-    del Hh, yh, nvh, sdh, truthh, r, rm
+    # counter-based Philox initial states (north_star's RNG; statistical parity)
+    ms, rp = timed(lambda: batched.detect_cim_batch(Hh, yh, nvh, ORDER, sdh,
+                                                    dataclasses.replace(prm, rng="philox")))
+    res["cfg3_16x16_16qam_slot_philox"] = {
+        "ms_per_slot": ms, "detections_per_s": P / ms * 1e3,
+        "ser": (rp.x_idx != truthh).any(-1).float().mean().item()}
+    del Hh, yh, nvh, sdh, truthh, r, rm, rp
     H, y, nv, sd, truth, _ = _synthetic_uplink(dev, P, 8, 16, 20.0, 11)
     ms, r = timed(lambda: batched.detect_cim_batch(H, y, nv, 16, sd, prm))
     res["cfg2_8x8_16qam_slot"] = {"ms_per_slot": ms, "detections_per_s": P / ms * 1e3,

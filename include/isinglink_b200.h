@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define IL_ABI_VERSION 1
+#define IL_ABI_VERSION 2
 
 enum il_status {
     IL_OK = 0,
@@ -62,7 +62,18 @@ typedef struct il_cac_params {
     double diverge_threshold; /*                                       (10.0) */
     double e_floor;           /*                                       (1e-6) */
     double init_amplitude;    /*                                       (0.1)  */
+    int32_t rng;              /* il_rng: initial-state generator              */
+    int32_t reserved;         /* must be 0                                    */
 } il_cac_params;
+
+/* Initial-state generator (solver.py:182-187 draws default_rng(derive_seed(
+ * seed, r)).uniform(-amp, amp, 2N + 1) per anneal r). */
+enum il_rng {
+    IL_RNG_NUMPY = 0,  /* those numpy streams, replayed bit for bit (SeedSequence + PCG64) */
+    IL_RNG_PHILOX = 1  /* counter-based Philox4x32-10 keyed by the same per-problem seed
+                          (csrc/rng_philox.cuh): FP32 states, no stream replay; parity is
+                          statistical against the reference */
+};
 
 /* Per-problem outcome of a batched detection (DetectionResult.source,
  * linear.py:33-41): "mmse" (the guess) = 0, "anneal" = 1, "mmse_sic" = 2

@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get(
 
 IL_OK, IL_ERR_ARG, IL_ERR_CUDA, IL_ERR_UNSUPPORTED, IL_ERR_NOMEM = 0, -1, -2, -3, -4
 PREC = {"fp64_exact": 0, "fp32": 1, "tf32": 2, "mixed": 3}
+RNG = {"numpy": 0, "philox": 1}
+ABI_VERSION = 2  # IL_ABI_VERSION of include/isinglink_b200.h (il_cac_params layout)
 
 _c_d = ctypes.c_double
 _c_i32 = ctypes.c_int32
@@ -30,6 +32,7 @@ class CacParamsC(ctypes.Structure):
         ("p", _c_d), ("a", _c_d), ("zeta", _c_d), ("eps", _c_d), ("dt", _c_d),
         ("f_mvm", _c_i32), ("n_steps", _c_i32), ("n_anneals", _c_i32), ("precision", _c_i32),
         ("diverge_threshold", _c_d), ("e_floor", _c_d), ("init_amplitude", _c_d),
+        ("rng", _c_i32), ("reserved", _c_i32),
     ]
 
 
@@ -107,6 +110,9 @@ def load(path: str = LIB_PATH):
                 fn = getattr(lib, name)
                 fn.argtypes = args
                 fn.restype = res
+            if lib.il_abi_version() != ABI_VERSION:
+                raise RuntimeError(f"{path} implements ABI {lib.il_abi_version()}, these bindings "
+                                   f"ABI {ABI_VERSION}: rebuild the library")
             _lib = lib
     return _lib
 

@@ -155,6 +155,8 @@ static int validate(const il_cac_params* p) {
                "diverge_threshold must exceed sqrt(max(a, p - 1)) = %.3g", floor_);
     IL_REQUIRE(p->precision >= IL_PREC_FP64_EXACT && p->precision <= IL_PREC_MIXED,
                "unknown precision %d", p->precision);
+    IL_REQUIRE(p->rng == IL_RNG_NUMPY || p->rng == IL_RNG_PHILOX, "unknown rng %d", p->rng);
+    IL_REQUIRE(p->reserved == 0, "il_cac_params.reserved must be 0");
     return IL_OK;
 }
 
@@ -171,6 +173,7 @@ static AnnealScalars scalars_of(const il_cac_params* p) {
     s.x0_range = p->init_amplitude - (-p->init_amplitude);  // numpy: high - low
     s.f_mvm = p->f_mvm;
     s.n_steps = p->n_steps;
+    s.rng = p->rng;
     return s;
 }
 

@@ -16,6 +16,7 @@
 // is generated on the device from the replayed NumPy streams.
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
+#include "rng_philox.cuh"
 
 namespace il {
 
@@ -67,6 +68,13 @@ k_anneal_exact(const double* __restrict__ Gall, const double* __restrict__ gall,
     if (x0all) {
         const double* x0 = x0all + (prob * B + r) * (int64_t)S;
         for (int i = 0; i < S; ++i) X[i * kLanes + lane] = x0[i];
+    } else if (s.rng == IL_RNG_PHILOX) {
+        for (int blk = 0; 4 * blk < S; ++blk) {
+            float v[4];
+            philox_x0_block(base_seed[prob], (uint32_t)r, (uint32_t)blk, (float)s.x0_lo,
+                            (float)s.x0_range, v);
+            for (int q = 0; q < 4 && 4 * blk + q < S; ++q) X[(4 * blk + q) * kLanes + lane] = v[q];
+        }
     } else {
         Pcg64 rng;
         rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)r));
@@ -196,6 +204,14 @@ k_anneal_exact_mw(const double* __restrict__ Gall, const double* __restrict__ ga
         if (x0all) {
             const double* x0 = x0all + (prob * B + r) * (int64_t)S;
             for (int i = s0; i < s1; ++i) X[i * kLanes + lane] = x0[i];
+        } else if (s.rng == IL_RNG_PHILOX) {  // counter-based: each warp its own spins
+            for (int blk = s0 / 4; 4 * blk < s1; ++blk) {
+                float v[4];
+                philox_x0_block(base_seed[prob], (uint32_t)r, (uint32_t)blk, (float)s.x0_lo,
+                                (float)s.x0_range, v);
+                for (int q = 0; q < 4; ++q)
+                    if (4 * blk + q >= s0 && 4 * blk + q < s1) X[(4 * blk + q) * kLanes + lane] = v[q];
+            }
         } else if (w == 0) {  // one stream per anneal, drawn in order
             Pcg64 rng;
             rng.seed_from(derive_seed2(base_seed[prob], (uint64_t)r));

@@ -97,6 +97,9 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
     fs.full_steps = full_steps_for(s.n_steps, precision);
     fs.n_probs = P;
     fs.gstats = gstats;
+    fs.rng = s.rng;
+    fs.x0_lo_f = (float)s.x0_lo;
+    fs.x0_range_f = (float)s.x0_range;
     IL_REQUIRE((steps == nullptr) == (mvms == nullptr) && (!steps || (count_rows > 0 && count_rows <= B)),
                "fast anneal: steps and mvms go together, for 1..B rows");
     // the screen pays off from N = 24 on (at N = 16 the FP64 epilogue is cheaper)

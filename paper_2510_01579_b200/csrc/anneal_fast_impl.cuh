@@ -51,6 +51,7 @@
 
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
+#include "rng_philox.cuh"
 #include "il_anneal.cuh"
 
 namespace il {
@@ -183,31 +184,51 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     uint4* frag = smem_u4 + warp * L::kWarpF4;      // G fragments (after x0 is consumed)
     float* x0s = reinterpret_cast<float*>(frag);    // x0 staging [16][S]
 
-    // ---- initial states: replayed NumPy streams, 2 lanes per anneal ---------
+    // ---- initial states: replayed NumPy streams (or Philox), 2 lanes per anneal
     {
         const int al = lane & 15, part = lane >> 4;
         const int a = PACK ? (al & 7) : mt * 16 + al;
-        Pcg64 rng;
-        rng.seed_from(derive_seed2(base_seed[PACK ? probh[al >> 3] : prob], (uint64_t)a));
-        // lane part 1 jumps ahead over the first half of the stream
-        if (part) rng.state = add128(mul128(rng.state, s.jump_mult[3]), mul128(rng.inc, s.jump_add[3]));
-        if constexpr (PAD) {
-            // stream draw i -> padded position (half A, half B, aux); the
-            // inert positions start at exactly 0
+        if (s.rng == IL_RNG_PHILOX) {
+            // counter-based: lane part p draws the 4-blocks p, p + 2, ...
             float* row = x0s + al * S;
-            for (int i = nr + part; i < N; i += 2) row[i] = row[N + i] = 0.f;
-            const int S0 = (Sg + 1) / 2;
-            const int i0 = part ? S0 : 0, i1 = part ? Sg : S0;
-            for (int i = i0; i < i1; ++i) {
-                const double u = rng.uniform(s.x0_lo, s.x0_range);
-                row[i < nr ? i : (i < 2 * nr ? N + i - nr : 2 * N)] = SC ? (float)(s.sdt * u) : (float)u;
+            if constexpr (PAD)
+                for (int i = nr + part; i < N; i += 2) row[i] = row[N + i] = 0.f;
+            const uint64_t sd = base_seed[PACK ? probh[al >> 3] : prob];
+            for (int blk = part; 4 * blk < Sg; blk += 2) {
+                float v[4];
+                philox_x0_block(sd, (uint32_t)a, (uint32_t)blk, s.x0_lo_f, s.x0_range_f, v);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int i = 4 * blk + q;
+                    if (i < Sg) {
+                        const int pos = !PAD ? i : (i < nr ? i : (i < 2 * nr ? N + i - nr : 2 * N));
+                        row[pos] = SC ? (float)(s.sdt * (double)v[q]) : v[q];
+                    }
+                }
             }
         } else {
-            constexpr int S0 = (S + 1) / 2;
-            const int i0 = part ? S0 : 0, i1 = part ? S : S0;
-            for (int i = i0; i < i1; ++i)
-                x0s[al * S + i] = SC ? (float)(s.sdt * rng.uniform(s.x0_lo, s.x0_range))
-                                     : (float)rng.uniform(s.x0_lo, s.x0_range);
+            Pcg64 rng;
+            rng.seed_from(derive_seed2(base_seed[PACK ? probh[al >> 3] : prob], (uint64_t)a));
+            // lane part 1 jumps ahead over the first half of the stream
+            if (part) rng.state = add128(mul128(rng.state, s.jump_mult[3]), mul128(rng.inc, s.jump_add[3]));
+            if constexpr (PAD) {
+                // stream draw i -> padded position (half A, half B, aux); the
+                // inert positions start at exactly 0
+                float* row = x0s + al * S;
+                for (int i = nr + part; i < N; i += 2) row[i] = row[N + i] = 0.f;
+                const int S0 = (Sg + 1) / 2;
+                const int i0 = part ? S0 : 0, i1 = part ? Sg : S0;
+                for (int i = i0; i < i1; ++i) {
+                    const double u = rng.uniform(s.x0_lo, s.x0_range);
+                    row[i < nr ? i : (i < 2 * nr ? N + i - nr : 2 * N)] = SC ? (float)(s.sdt * u) : (float)u;
+                }
+            } else {
+                constexpr int S0 = (S + 1) / 2;
+                const int i0 = part ? S0 : 0, i1 = part ? S : S0;
+                for (int i = i0; i < i1; ++i)
+                    x0s[al * S + i] = SC ? (float)(s.sdt * rng.uniform(s.x0_lo, s.x0_range))
+                                         : (float)rng.uniform(s.x0_lo, s.x0_range);
+            }
         }
     }
 

@@ -38,6 +38,8 @@ struct FastScalars {
     int full_steps;  // refreshes at steps < full_steps take the lo(v) x hi(G) pass too
     int64_t n_probs; // problems in the launch (PACK: the last warp may hold one)
     const double* gstats;  // [P][2] max |G|, sum |G| + sum |b| from the front end, or null
+    int rng;               // il_rng
+    float x0_lo_f, x0_range_f;  // IL_RNG_PHILOX: FP32 x0 = fmaf(range, u, lo)
 };
 
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }

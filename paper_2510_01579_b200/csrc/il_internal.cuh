@@ -10,6 +10,7 @@ struct AnnealScalars {
     double p, a, zeta, eps, dt, e_floor, thr;
     double x0_lo, x0_range;  // uniform(lo, lo + range): lo = -amp, range = amp - (-amp)
     int f_mvm, n_steps;
+    int rng = 0;  // il_rng
 };
 
 // ---- anneal kernels --------------------------------------------------------

@@ -136,6 +136,8 @@ int il_solve_batch(const double* G, const double* g_diag, const double* b, const
     s.x0_range = prm->init_amplitude - (-prm->init_amplitude);
     s.f_mvm = prm->f_mvm;
     s.n_steps = prm->n_steps;
+    IL_REQUIRE(prm->rng == IL_RNG_NUMPY || prm->rng == IL_RNG_PHILOX, "unknown rng %d", prm->rng);
+    s.rng = prm->rng;
     int rc = IL_OK;
     Workspace ws(st);
     // counters (steps / mvms) are reported by both kernels, so asking for
@@ -192,6 +194,8 @@ int il_integrate_batch(const double* G, const double* g_diag, const double* b, c
     s.x0_range = prm->init_amplitude - (-prm->init_amplitude);
     s.f_mvm = prm->f_mvm;
     s.n_steps = prm->n_steps;
+    IL_REQUIRE(prm->rng == IL_RNG_NUMPY || prm->rng == IL_RNG_PHILOX, "unknown rng %d", prm->rng);
+    s.rng = prm->rng;
     int rc = IL_OK;
     Workspace ws(st);
     double* x0 = ws.get<double>((size_t)P * S, &rc);

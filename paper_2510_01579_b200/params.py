@@ -13,6 +13,12 @@ the B200 arithmetic mode.
     (G split to FP32 accuracy, the state rounded to f16): the early steps,
     where the chaotic dynamics amplify rounding, keep FP32 accuracy.
 
+``rng`` selects the initial states: ``"numpy"`` (default) replays the
+reference's numpy streams bit for bit; ``"philox"`` draws them from a
+counter-based Philox4x32-10 keyed by the same per-problem seeds (cheaper,
+statistically equivalent; with ``precision="fp64_exact"`` it gives the FP64
+reference dynamics on the same states).
+
 Reference ``CacParams`` objects (no ``precision`` attribute) are accepted
 everywhere and run in ``DEFAULT_PRECISION``.
 """
@@ -23,7 +29,7 @@ import math
 import os
 from dataclasses import dataclass
 
-from ._lib import PREC, CacParamsC
+from ._lib import PREC, RNG, CacParamsC
 
 DEFAULT_PRECISION = os.environ.get("ISINGLINK_B200_PRECISION", "fp32")
 if DEFAULT_PRECISION not in PREC:
@@ -45,6 +51,7 @@ class CacParams:
     e_floor: float = 1e-6
     init_amplitude: float = 0.1
     precision: str = DEFAULT_PRECISION
+    rng: str = "numpy"
 
     def validate(self) -> None:
         """Same rules and messages as the reference (solver.py:109-124)."""
@@ -64,6 +71,8 @@ class CacParams:
                 f"diverge_threshold must exceed sqrt(max(a, p - 1)) = {floor:.3g}")
         if self.precision not in PREC:
             raise ValueError(f"precision must be one of {sorted(PREC)}")
+        if self.rng not in RNG:
+            raise ValueError(f"rng must be one of {sorted(RNG)}")
 
 
 def precision_of(params) -> str:
@@ -83,4 +92,5 @@ def to_c(params, precision: str | None = None) -> CacParamsC:
                       n_anneals=int(params.n_anneals), precision=PREC[prec],
                       diverge_threshold=float(params.diverge_threshold),
                       e_floor=float(params.e_floor),
-                      init_amplitude=float(params.init_amplitude))
+                      init_amplitude=float(params.init_amplitude),
+                      rng=RNG[getattr(params, "rng", "numpy") or "numpy"], reserved=0)

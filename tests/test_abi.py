@@ -1,5 +1,6 @@
 """The C-ABI library loads on CPU and exports every symbol include/*.h declares."""
 
+import ctypes
 import glob
 import os
 import re
@@ -36,7 +37,8 @@ def test_library_exports_every_declared_symbol(built_lib):
 def test_library_loads_without_gpu(built_lib):
     from paper_2510_01579_b200 import _lib
     lib = _lib.load()
-    assert lib.il_abi_version() == 1
+    assert lib.il_abi_version() == _lib.ABI_VERSION == 2
+    assert ctypes.sizeof(_lib.CacParamsC) == 88  # il_cac_params
     assert isinstance(lib.il_last_error(), bytes)
 
 
