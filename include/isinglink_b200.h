@@ -167,6 +167,11 @@ int il_build_ising_batch(const double* H, const double* y, const uint8_t* guess_
 int il_spin_energies(const double* G, const double* g_diag, const double* b,
                      const int8_t* spins, int64_t P, int32_t n_batch, int32_t n_dim,
                      double* energies, void* stream);
+/* structured_mvm (solver.py:147-168) for P problems: v = x1 + x2,
+ * out[P][2N+1] = [G v - g x1 + b xa, G v - g x2 + b xa, b.v] (FP64). */
+int il_structured_mvm_batch(const double* G, const double* g_diag, const double* b,
+                            const double* x1, const double* x2, const double* xa, int64_t P,
+                            int32_t n_dim, double* out, void* stream);
 int il_solve_batch(const double* G, const double* g_diag, const double* b,
                    const double* offset, const double* fallback_energy, const double* eps,
                    const uint64_t* base_seed, int64_t P, int32_t n_dim,
@@ -294,6 +299,11 @@ int il_precode_vpp_host(const double* H, const double* u, int64_t P, int32_t n_u
  * complex128 perturbation (even Gaussian integers), unnorm_power[P],
  * diverged_count[P] (may be NULL).
  * ------------------------------------------------------------------------- */
+/* Zero forcing (precoder.py:54-60) for P channels: W[P][n_ant][n_u] =
+ * H^H (H H^H)^-1 by Cholesky; status[p] = -1 where the Cholesky broke down
+ * (the reference raises LinAlgError). */
+int il_zf_batch(const double* H, int64_t P, int32_t n_u, int32_t n_ant, double* W,
+                int8_t* status, void* stream);
 int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_u,
                          int32_t n_ant, double power, double tau, int32_t n_stages,
                          const uint64_t* seed, const il_cac_params* prm, double* x,

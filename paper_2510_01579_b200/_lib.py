@@ -81,6 +81,9 @@ _SIGS = {
                              ctypes.c_int),
     "il_gray_demap": ([_vp, _c_i64, _c_i32, _vp, _vp], ctypes.c_int),
     "il_spin_energies": ([_vp, _vp, _vp, _vp, _c_i64, _c_i32, _c_i32, _vp, _vp], ctypes.c_int),
+    "il_structured_mvm_batch": ([_vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32, _vp, _vp],
+                                ctypes.c_int),
+    "il_zf_batch": ([_vp, _c_i64, _c_i32, _c_i32, _vp, _vp, _vp], ctypes.c_int),
     "il_solve_batch": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp, _c_i64, _c_i32,
                         ctypes.POINTER(CacParamsC), _vp, _vp, _vp, _vp, _vp, _vp, _vp],
                        ctypes.c_int),

@@ -22,7 +22,8 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from . import batched
+from . import _lib, batched
+from .batched import _stream
 from .channel import (Constellation, MimoInstance, from_indices, make_qam,  # noqa: F401
                       project_to_constellation, to_indices)
 from .params import CacParams
@@ -238,14 +239,18 @@ def structured_mvm(si: StructuredIsing, x1, x2, xa: float) -> np.ndarray:
     x2 = np.asarray(x2, dtype=np.float64)
     if x1.shape != (si.n_dim,) or x2.shape != (si.n_dim,):
         raise ValueError("x1/x2 must have length n_dim")
-    G = torch.as_tensor(si.G, device="cuda")
-    g = torch.as_tensor(si.g_diag, device="cuda")
-    b = torch.as_tensor(si.b, device="cuda")
-    t1 = torch.as_tensor(x1, device="cuda")
-    t2 = torch.as_tensor(x2, device="cuda")
-    v = t1 + t2
-    m = G @ v
-    out = torch.cat([m - g * t1 + b * xa, m - g * t2 + b * xa, (b @ v)[None]])
+    N = si.n_dim
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f64 = dict(dtype=torch.float64, device=dev)
+    G = torch.as_tensor(np.ascontiguousarray(si.G, dtype=np.float64), **f64)
+    g = torch.as_tensor(np.ascontiguousarray(si.g_diag, dtype=np.float64), **f64)
+    b = torch.as_tensor(np.ascontiguousarray(si.b, dtype=np.float64), **f64)
+    t1 = torch.as_tensor(x1, **f64)
+    t2 = torch.as_tensor(x2, **f64)
+    ta = torch.tensor([float(xa)], **f64)
+    out = torch.empty(2 * N + 1, **f64)
+    _lib.call("il_structured_mvm_batch", G.data_ptr(), g.data_ptr(), b.data_ptr(), t1.data_ptr(),
+              t2.data_ptr(), ta.data_ptr(), 1, N, out.data_ptr(), _stream())
     return out.cpu().numpy()
 
 
@@ -391,10 +396,14 @@ def zf_matrix(H: np.ndarray) -> np.ndarray:
     n_r, n_t = H.shape
     if n_r > n_t:
         raise ValueError("downlink precoding requires n_r <= n_t")
-    Ht = torch.as_tensor(np.asarray(H, dtype=complex), device="cuda")
-    A = Ht @ Ht.conj().T
-    L = torch.linalg.cholesky(A)
-    return torch.cholesky_solve(Ht, L).conj().T.cpu().numpy()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    Ht = torch.as_tensor(np.ascontiguousarray(H, dtype=np.complex128), device=dev)
+    W = torch.empty((n_t, n_r), dtype=torch.complex128, device=dev)
+    status = torch.empty(1, dtype=torch.int8, device=dev)
+    _lib.call("il_zf_batch", Ht.data_ptr(), 1, n_r, n_t, W.data_ptr(), status.data_ptr(), _stream())
+    if int(status.item()) != 0:
+        raise np.linalg.LinAlgError("H H^H is not positive definite")
+    return W.cpu().numpy()
 
 
 def precode_zf(H: np.ndarray, u: np.ndarray, P: float) -> np.ndarray:

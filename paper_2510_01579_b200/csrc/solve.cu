@@ -37,6 +37,35 @@ __global__ void k_spin_energies(const double* __restrict__ Gg, const double* __r
     }
 }
 
+// Coupling field of solver.py:147-168 for P problems: v = x1 + x2, m = G v,
+// out = [m - g x1 + b xa, m - g x2 + b xa, b.v].  One warp per problem, lane
+// i (+32..) owns row i; the row sum runs over j in order.
+__global__ void k_structured_mvm(const double* __restrict__ Gg, const double* __restrict__ gg,
+                                 const double* __restrict__ bg, const double* __restrict__ x1g,
+                                 const double* __restrict__ x2g, const double* __restrict__ xag,
+                                 int64_t P, int N, double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t prob = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (prob >= P) return;
+    const double* G = Gg + prob * (int64_t)N * N;
+    const double* x1 = x1g + prob * N;
+    const double* x2 = x2g + prob * N;
+    const double* b = bg + prob * N;
+    const double* gd = gg + prob * N;
+    const double xa = xag[prob];
+    double* o = out + prob * (int64_t)(2 * N + 1);
+    double bv = 0.0;
+    for (int i = lane; i < N; i += 32) {
+        double m = 0.0;
+        for (int j = 0; j < N; ++j) m = fma(G[(int64_t)i * N + j], x1[j] + x2[j], m);
+        o[i] = (m - gd[i] * x1[i]) + b[i] * xa;
+        o[N + i] = (m - gd[i] * x2[i]) + b[i] * xa;
+        bv = fma(b[i], x1[i] + x2[i], bv);
+    }
+    bv = warp_sum(bv);
+    if (lane == 0) o[2 * N] = bv;
+}
+
 // Best non-diverged anneal (strict <, lowest index wins), fallback test,
 // and the winner's spins.  One warp per problem.
 __global__ void k_select_best(const double* __restrict__ energies, const uint8_t* __restrict__ div,
@@ -111,6 +140,38 @@ int il_spin_energies(const double* G, const double* g_diag, const double* b, con
     (void)g_diag;  // tr G is read from G's diagonal, as the reference sums g_diag = diag(G)
     IL_REQUIRE(P >= 0 && n_batch >= 0 && n_dim >= 0, "negative shape");
     return launch_spin_energies(G, b, spins, P, n_batch, n_dim, energies, (cudaStream_t)stream);
+}
+
+int il_structured_mvm_batch(const double* G, const double* g_diag, const double* b,
+                            const double* x1, const double* x2, const double* xa, int64_t P,
+                            int32_t n_dim, double* out, void* stream) {
+    IL_REQUIRE(P >= 0 && n_dim >= 1, "invalid shape");
+    if (P == 0) return IL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int wpb = 4;
+    IL_LAUNCH(kProfOther, st, k_structured_mvm<<<(unsigned)((P + wpb - 1) / wpb), 32 * wpb, 0, st>>>(
+                                  G, g_diag, b, x1, x2, xa, P, n_dim, out););
+    IL_CHECK_CUDA(cudaGetLastError());
+    return IL_OK;
+}
+
+int il_zf_batch(const double* H, int64_t P, int32_t n_u, int32_t n_ant, double* W, int8_t* status,
+                void* stream) {
+    IL_REQUIRE(P >= 0 && n_u >= 1 && n_ant >= n_u && n_ant <= 32,
+               "zero forcing requires 1 <= n_u <= n_ant <= 32");
+    IL_REQUIRE(P == 0 || (H && W && status), "NULL buffer");
+    if (P == 0) return IL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace ws(st);
+    int rc = IL_OK;
+    // the VPP front end's ZF stage, with the symbol-dependent outputs discarded
+    double* u = ws.get<double>((size_t)P * n_u * 2, &rc);
+    double* y_t = ws.get<double>((size_t)P * n_ant * 2, &rc);
+    double* H_p = ws.get<double>((size_t)P * n_ant * n_u * 2, &rc);
+    double* base = ws.get<double>((size_t)P, &rc);
+    if (rc) return rc;
+    IL_CHECK_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * (size_t)P * n_u * 2, st));
+    return launch_zf_vpp_front(H, u, P, n_u, n_ant, 0.0, W, y_t, H_p, base, status, st);
 }
 
 int il_solve_batch(const double* G, const double* g_diag, const double* b, const double* offset,
