@@ -462,6 +462,7 @@ int il_detect_cim_multi_batch(const double* H, const double* y, const double* no
     double* off = ws.get<double>((size_t)P, &rc);
     double* eps = ws.get<double>((size_t)P, &rc);
     uint64_t* base = ws.get<uint64_t>((size_t)P, &rc);
+    double* gstats = front_rows_supported(n_r, n_t) ? ws.get<double>((size_t)P * 2, &rc) : nullptr;
     if (rc) return rc;
     IL_CHECK_CUDA(cudaMemcpyAsync(codes, chains, sizeof(int32_t) * n_chains,
                                   cudaMemcpyHostToDevice, st));
@@ -486,13 +487,13 @@ int il_detect_cim_multi_batch(const double* H, const double* y, const double* no
         IL_CHECK_CUDA(cudaMemsetAsync(widx, 0xff, sizeof(int32_t) * P, st));  // -1
         for (int stage = 0; stage < n_stages; ++stage) {
             rc = launch_build_ising(H, y, gx, P, n_r, n_t, al, G, g, b, off, nullptr, eps, 1.0,
-                                    fixed, st);
+                                    fixed, st, gstats);
             if (rc) return rc;
             rc = launch_base_seeds(seed, P, (uint64_t)c, (uint64_t)stage, base, st);
             if (rc) return rc;
             IL_CHECK_CUDA(cudaMemsetAsync(ssrc, 0, (size_t)P, st));
             rc = anneal_and_select(H, y, P, n_r, n_t, al, G, g, b, off, eps, base, prm, gx, ge,
-                                   ssrc, sai, sdc, st);
+                                   ssrc, sai, sdc, st, gstats);
             if (rc) return rc;
             rc = launch_multi_stage(sai, P, widx, st);
             if (rc) return rc;
@@ -537,6 +538,7 @@ int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_
     double* eps = ws.get<double>((size_t)P, &rc);
     uint64_t* base = ws.get<uint64_t>((size_t)P, &rc);
     int32_t* stage_div = diverged_count ? ws.get<int32_t>((size_t)P, &rc) : nullptr;
+    double* gstats = front_rows_supported(n_ant, n_u) ? ws.get<double>((size_t)P * 2, &rc) : nullptr;
     if (rc) return rc;
     rc = launch_zf_vpp_front(H, u, P, n_u, n_ant, tau, W, yt, Hp, base_e, status, st);
     if (rc) return rc;
@@ -547,12 +549,12 @@ int il_precode_vpp_batch(const double* H, const double* u, int64_t P, int32_t n_
     for (int stage = 0; stage < n_stages; ++stage) {
         // precoder.py:115-124: _improve_guess(..., derive_seed(seed, 0, stage), eps_gain=1/16)
         rc = launch_build_ising(Hp, yt, vidx, P, n_ant, n_u, al, G, g, b, off, nullptr, eps,
-                                0.0625, fixed, st);
+                                0.0625, fixed, st, gstats);
         if (rc) return rc;
         rc = launch_base_seeds(seed, P, 0, (uint64_t)stage, base, st);
         if (rc) return rc;
         rc = anneal_and_select(Hp, yt, P, n_ant, n_u, al, G, g, b, off, eps, base, prm, vidx, en,
-                               nullptr, nullptr, stage_div, st);
+                               nullptr, nullptr, stage_div, st, gstats);
         if (rc) return rc;
         if (diverged_count) {
             rc = launch_add_i32(stage_div, P, diverged_count, st);

@@ -751,9 +751,11 @@ int launch_mmse(const double* H, const double* y, const double* noise_var, int64
 int launch_build_ising(const double* H, const double* y, const uint8_t* guess_idx, int64_t P,
                        int n_r, int n_t, const Alphabet& al, double* G, double* g_diag,
                        double* b, double* offset, double* eps_scale, double* eps_out,
-                       double eps_gain, double fixed_eps, cudaStream_t st) {
+                       double eps_gain, double fixed_eps, cudaStream_t st, double* gstats) {
     if (P == 0) return IL_OK;
     IsingOut o{G, g_diag, b, offset, eps_scale, eps_out, eps_gain, fixed_eps};
+    IL_REQUIRE(!gstats || front_rows_supported(n_r, n_t), "gstats come from the row front end only");
+    o.gstats = gstats;
     if (front_rows_supported(n_r, n_t))
         return launch_front_rows(false, true, H, y, nullptr, P, n_r, n_t, al,
                                  const_cast<uint8_t*>(guess_idx), nullptr, nullptr, o, st);

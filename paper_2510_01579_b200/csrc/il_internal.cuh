@@ -86,7 +86,7 @@ int launch_mmse(const double* H, const double* y, const double* noise_var, int64
 int launch_build_ising(const double* H, const double* y, const uint8_t* guess_idx, int64_t P,
                        int n_r, int n_t, const Alphabet& al, double* G, double* g_diag,
                        double* b, double* offset, double* eps_scale, double* eps_out,
-                       double eps_gain, double fixed_eps, cudaStream_t st);
+                       double eps_gain, double fixed_eps, cudaStream_t st, double* gstats = nullptr);
 // VPP front-end: W = H^H (H H^H)^-1 [n_ant x n_u], y_t = W u, H_p = -tau/2 W,
 // base energy ||y_t||^2.  status[p] = -1 on Cholesky breakdown.
 int launch_zf_vpp_front(const double* H, const double* u, int64_t P, int n_u, int n_ant,
