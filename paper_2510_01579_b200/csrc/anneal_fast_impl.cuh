@@ -260,8 +260,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
 #pragma unroll 4
             for (int i = lane; i < nr * nr; i += 32) gmax = fmax(gmax, fabs(__ldg(Gp + i)));
         }
+        if (!s.gstats) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+            for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
+        }
         int ex = 0;
         frexp(K * gmax, &ex);
         const int sc = (K * gmax > 0.0) ? 8 - ex : 0;
