@@ -365,6 +365,20 @@ def other_configs(dev, prm) -> dict:
         sweep[str(na)] = {"ms_per_slot": ms, "detections_per_s": P / ms * 1e3,
                           "ser": (r.x_idx != truth).any(-1).float().mean().item()}
     res["cfg5_16x16_64qam_30db_replica_sweep_per_slot"] = sweep
+    del H, y, nv, sd, truth
+    # BASELINE.json config 5 proper: a 20-slot batch (917,280 REs) per call
+    P20 = 20 * P
+    H, y, nv, sd, truth, _ = _synthetic_uplink(dev, P20, 16, 64, 30.0, 15)
+    batch20 = {}
+    for na in (8, 16, 32, 64, 128):
+        p2 = dataclasses.replace(prm, n_anneals=na)
+        ms, r = timed(lambda: batched.detect_cim_batch(H, y, nv, 64, sd, p2))
+        batch20[str(na)] = {"ms_per_20_slots": ms, "detections_per_s": P20 / ms * 1e3,
+                            "ser": (r.x_idx != truth).any(-1).float().mean().item()}
+        del r
+    res["cfg5_16x16_64qam_30db_20slot_batch_replica_sweep"] = batch20
+    del H, y, nv, sd, truth
+    torch.cuda.empty_cache()
     return res
 
 

@@ -307,14 +307,16 @@ def _detect(name: str, b: dict, cfg, prm: CacParams):
     return r.x_idx, r.energy, r.diverged, r.source
 
 
-def run_detection_sweep(cfg, precision: str = "fp64_exact") -> list:
-    """Paired uplink sweep (sweeps.py:150-192), every detector on the GPU."""
+def run_detection_sweep(cfg, precision: str = "fp64_exact", rng: str = "numpy") -> list:
+    """Paired uplink sweep (sweeps.py:150-192), every detector on the GPU.
+    ``rng="philox"`` draws the anneals' initial states from Philox4x32-10
+    instead of the reference's numpy streams (statistical parity)."""
     cfg.validate()
     if cfg.mode != "uplink_sweep":
         raise ValueError(f"config mode is {cfg.mode!r}, expected uplink_sweep")
     const = make_qam(cfg.modulation)
     bpd = int(round(math.log2(int(math.isqrt(cfg.modulation)))))
-    prm = dataclasses.replace(_params(cfg), precision=precision)
+    prm = dataclasses.replace(_params(cfg), precision=precision, rng=rng)
     n_sym = cfg.n_trials * cfg.n_t
     n_bit = n_sym * const.bits_per_symbol
     rows = []
@@ -346,7 +348,7 @@ def run_detection_sweep(cfg, precision: str = "fp64_exact") -> list:
 # ---------------------------------------------------------------------------
 # downlink sweep (sweeps.py:195-279)
 # ---------------------------------------------------------------------------
-def run_precoding_sweep(cfg, precision: str = "fp64_exact") -> list:
+def run_precoding_sweep(cfg, precision: str = "fp64_exact", rng: str = "numpy") -> list:
     """Paired downlink sweep: ZF vs VPP through a modulo-tau receiver.
 
     VPP runs batched on the GPU (precoder.py:93-146); ZF and the receiver
@@ -359,7 +361,7 @@ def run_precoding_sweep(cfg, precision: str = "fp64_exact") -> list:
     const = make_qam(cfg.modulation)
     tau = api.default_tau(const)
     P = cfg.power if cfg.power > 0 else float(cfg.n_r)
-    prm = dataclasses.replace(_params(cfg), precision=precision)
+    prm = dataclasses.replace(_params(cfg), precision=precision, rng=rng)
     n_sym = cfg.n_trials * cfg.n_r
     n_bit = n_sym * const.bits_per_symbol
     rows = []

@@ -90,23 +90,29 @@ def harness(built_lib):
     return harness
 
 
-@pytest.mark.parametrize("precision", ["fp64_exact", "fp32"])
+# (precision, initial states): the FP64-exact mode reproduces the tables; the
+# throughput modes -- FP32, mixed, and FP32 with Philox initial states
+# (SURVEY 8(c) gate 4) -- land inside each point's binomial 95% CI
+MODES = [("fp64_exact", "numpy"), ("fp32", "numpy"), ("mixed", "numpy"), ("fp32", "philox")]
+
+
+@pytest.mark.parametrize("precision,rng", MODES)
 @pytest.mark.parametrize("name", sorted(TABLES))
-def test_uplink_curves(name, precision, harness):
+def test_uplink_curves(name, precision, rng, harness):
     over, table = TABLES[name]
     cfg = dataclasses.replace(harness.ExperimentConfig(), mode="uplink_sweep", seed=1,
                               detectors=tuple(table), **over)
-    rows = harness.run_detection_sweep(cfg, precision=precision)
+    rows = harness.run_detection_sweep(cfg, precision=precision, rng=rng)
     bps = int(round(math.log2(cfg.modulation)))
     n_sym = cfg.n_trials * cfg.n_t
     _check(rows, table, n_sym, n_sym * bps, "exact" if precision == "fp64_exact" else "ci")
 
 
-@pytest.mark.parametrize("precision", ["fp64_exact", "fp32"])
-def test_downlink_curves(precision, harness):
+@pytest.mark.parametrize("precision,rng", MODES)
+def test_downlink_curves(precision, rng, harness):
     over, table = DOWNLINK
     cfg = dataclasses.replace(harness.ExperimentConfig(), seed=1, **over)
-    rows = harness.run_precoding_sweep(cfg, precision=precision)
+    rows = harness.run_precoding_sweep(cfg, precision=precision, rng=rng)
     n_sym = cfg.n_trials * cfg.n_r
     _check(rows, table, n_sym, n_sym * 4, "exact" if precision == "fp64_exact" else "ci")
 
@@ -121,14 +127,14 @@ def test_ml_floor_cfg1(harness):
         assert abs(r.ser - float(want[r.snr_db])) <= _half_ulp(want[r.snr_db]) * 1.0001, r
 
 
-@pytest.mark.parametrize("precision", ["fp64_exact", "fp32"])
-def test_replica_sweep_cfg5(precision, harness):
+@pytest.mark.parametrize("precision,rng", MODES)
+def test_replica_sweep_cfg5(precision, rng, harness):
     base = dataclasses.replace(harness.ExperimentConfig(), mode="uplink_sweep", seed=1, n_r=16,
                                n_t=16, modulation=64, snr_grid_db=(30.0,), n_trials=800,
                                detectors=("cim",))
     for na, (ser_s, ber_s) in REPLICA.items():
         cfg = dataclasses.replace(base, cac=dataclasses.replace(base.cac, n_anneals=na))
-        (r,) = harness.run_detection_sweep(cfg, precision=precision)
+        (r,) = harness.run_detection_sweep(cfg, precision=precision, rng=rng)
         n_sym = 800 * 16
         _check([r], {"cim": [(ser_s, ber_s)]}, n_sym, n_sym * 6,
                "exact" if precision == "fp64_exact" else "ci")
