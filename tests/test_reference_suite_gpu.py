@@ -33,7 +33,7 @@ ACTIVE_FILES = ["test_solver.py", "test_transform.py", "test_detector.py", "test
                 "test_linear.py", "test_channel.py", "test_harness.py"]
 
 
-def _run(files, activate: bool, timeout=900, verbose=False):
+def _run(files, activate: bool, timeout=900, verbose=False, extra=()):
     if not (os.path.isdir(REF_TESTS) and os.path.isdir(REF_PKG)):
         pytest.fail("reference suite not staged: run `make -C oracle refpkg` in the build "
                     "container (it needs /root/reference)")
@@ -42,7 +42,7 @@ def _run(files, activate: bool, timeout=900, verbose=False):
                                          env.get("PYTHONPATH", "")])
     env["ISINGLINK_REF_ACTIVATE"] = "1" if activate else "0"
     cmd = [sys.executable, "-m", "pytest", "-v" if verbose else "-q", "-p", "ref_suite_plugin", "-p",
-           "no:cacheprovider", "-c", os.devnull, "--rootdir", REF_TESTS, *files]
+           "no:cacheprovider", "-c", os.devnull, "--rootdir", REF_TESTS, *extra, *files]
     r = subprocess.run(cmd, cwd=REF_TESTS, env=env, capture_output=True, text=True,
                        timeout=timeout)
     tail = "\n".join((r.stdout + r.stderr).strip().splitlines()[-25:])
@@ -60,6 +60,17 @@ def test_reference_backend_suite_with_cuda_registered(built_lib):
 @pytest.mark.parametrize("name", ACTIVE_FILES)
 def test_reference_suite_with_cuda_active(built_lib, name):
     _run([name], activate=True)
+
+
+def test_reference_acceptance_criteria_with_cuda_active(built_lib):
+    """The reference's acceptance suite (test_acceptance.py:67-429), criteria
+    1-7 and 9, with every anneal of its own code path on the CUDA plugin
+    (about 2 minutes).  Criterion 8 times the reference's CPU worker pool
+    (1 -> 2 -> 4 processes), not the kernel, and is left out."""
+    out = _run(["test_acceptance.py"], activate=True, timeout=1800, verbose=True,
+               extra=("-s", "-k", "not criterion_08"))
+    for c in (1, 2, 3, 4, 5, 6, 7, 9):
+        assert f"ACCEPTANCE criterion {c}: PASS" in out, c
 
 
 def test_cuda_agrees_bit_for_bit_with_reference_kernel(built_lib):
