@@ -77,10 +77,15 @@ def _check(rows, table, n_sym, n_bit, mode):
             r = by[(det, snr)]
             for got, want_s, n in ((r.ser, ser_s, n_sym), (r.ber, ber_s, n_bit)):
                 want = float(want_s)
+                var = max(want * (1 - want), 1.0 / n) / n
                 if mode == "exact":
                     assert abs(got - want) <= _half_ulp(want_s) * 1.0001, (det, snr, got, want_s)
-                else:  # binomial 95% CI of the reference value (+ rounding of the table)
-                    ci = 1.96 * math.sqrt(max(want * (1 - want), 1.0 / n) / n) + _half_ulp(want_s)
+                elif mode == "ci":  # binomial 95% CI of the reference value (+ rounding of the table)
+                    ci = 1.96 * math.sqrt(var) + _half_ulp(want_s)
+                    assert abs(got - want) <= ci, (det, snr, got, want_s, ci)
+                else:  # "independent": other initial states, so a second binomial sample;
+                    # two-sample test at 99.9% per point (about 99% over a table)
+                    ci = 3.29 * math.sqrt(2.0 * var) + _half_ulp(want_s)
                     assert abs(got - want) <= ci, (det, snr, got, want_s, ci)
 
 
@@ -91,9 +96,18 @@ def harness(built_lib):
 
 
 # (precision, initial states): the FP64-exact mode reproduces the tables; the
-# throughput modes -- FP32, mixed, and FP32 with Philox initial states
-# (SURVEY 8(c) gate 4) -- land inside each point's binomial 95% CI
+# FP32 and mixed modes, on the reference's own initial states, land inside
+# each point's binomial 95% CI.  With Philox initial states (SURVEY 8(c) gate
+# 4) the anneals are a different random sample: at high SNR the CIM's errors
+# are mostly anneal outcomes, so the SER is a second, independent binomial
+# draw and the gate is a two-sample test (tools/rng_ser_probe.py: on 2 x 10^5
+# REs per configuration the numpy-stream and Philox SERs differ by no more
+# than two seedings of the same generator).
 MODES = [("fp64_exact", "numpy"), ("fp32", "numpy"), ("mixed", "numpy"), ("fp32", "philox")]
+
+
+def _mode(precision, rng):
+    return "exact" if precision == "fp64_exact" else ("ci" if rng == "numpy" else "independent")
 
 
 @pytest.mark.parametrize("precision,rng", MODES)
@@ -105,7 +119,7 @@ def test_uplink_curves(name, precision, rng, harness):
     rows = harness.run_detection_sweep(cfg, precision=precision, rng=rng)
     bps = int(round(math.log2(cfg.modulation)))
     n_sym = cfg.n_trials * cfg.n_t
-    _check(rows, table, n_sym, n_sym * bps, "exact" if precision == "fp64_exact" else "ci")
+    _check(rows, table, n_sym, n_sym * bps, _mode(precision, rng))
 
 
 @pytest.mark.parametrize("precision,rng", MODES)
@@ -114,7 +128,7 @@ def test_downlink_curves(precision, rng, harness):
     cfg = dataclasses.replace(harness.ExperimentConfig(), seed=1, **over)
     rows = harness.run_precoding_sweep(cfg, precision=precision, rng=rng)
     n_sym = cfg.n_trials * cfg.n_r
-    _check(rows, table, n_sym, n_sym * 4, "exact" if precision == "fp64_exact" else "ci")
+    _check(rows, table, n_sym, n_sym * 4, _mode(precision, rng))
 
 
 def test_ml_floor_cfg1(harness):
@@ -136,5 +150,4 @@ def test_replica_sweep_cfg5(precision, rng, harness):
         cfg = dataclasses.replace(base, cac=dataclasses.replace(base.cac, n_anneals=na))
         (r,) = harness.run_detection_sweep(cfg, precision=precision, rng=rng)
         n_sym = 800 * 16
-        _check([r], {"cim": [(ser_s, ber_s)]}, n_sym, n_sym * 6,
-               "exact" if precision == "fp64_exact" else "ci")
+        _check([r], {"cim": [(ser_s, ber_s)]}, n_sym, n_sym * 6, _mode(precision, rng))
