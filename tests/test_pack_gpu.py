@@ -49,10 +49,11 @@ def _both(fn):
 # (N = 16), inert padding spins (n_t = 6, 10), fewer than 8 anneals, odd P
 # (the last warp holds a single problem)
 CASES = [(16, 64, 30.0, 8, 2001), (8, 16, 20.0, 8, 1537), (6, 16, 15.0, 5, 999),
-         (10, 4, 10.0, 8, 1024), (16, 16, 20.0, 3, 777)]
+         (10, 4, 10.0, 8, 1024), (16, 16, 20.0, 3, 777), (1, 4, 10.0, 8, 257),
+         (24, 16, 20.0, 8, 301), (32, 4, 15.0, 8, 129)]
 
 
-@pytest.mark.parametrize("precision", ["fp32", "mixed"])
+@pytest.mark.parametrize("precision", ["fp32", "mixed", "tf32"])
 @pytest.mark.parametrize("n_t,order,snr,n_anneals,P", CASES)
 def test_detect_cim_packed_equals_padded(n_t, order, snr, n_anneals, P, precision):
     import bench
