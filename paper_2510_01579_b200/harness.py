@@ -468,6 +468,53 @@ def run_integration_heatmap(cfg) -> list:
 # ---------------------------------------------------------------------------
 # benchmark report (bench.py:147-203), GPU form
 # ---------------------------------------------------------------------------
+def kernel_comparison(isinglink, cfg, n_probe: int = 64) -> dict:
+    """The reference's ``_kernel_comparison`` (harness/bench.py:117-144) with
+    the CUDA plugin among the kernels.
+
+    ``isinglink`` is the reference package with ``install(isinglink)`` done.
+    Every available kernel ("cuda", "ext", "python") times ``detect_cim`` per
+    instance through the reference's own code path on the reference bench's
+    instances and seeds; each kernel's decisions are compared with "ext".
+    The batched slot path (``batched.detect_cim_batch``, P = n_probe in one
+    call, FP64-exact and FP32) is timed and compared beside them."""
+    from isinglink.harness.bench import _DOM_BENCH, _bench_instances  # reference internals
+    cfg.validate()
+    instances = _bench_instances(cfg)[:n_probe]
+    timings, outputs = {}, {}
+    for name in sorted(isinglink.available_kernels()):
+        with isinglink.use_kernel(name):
+            t0 = time.perf_counter()
+            res = [isinglink.detect_cim(inst, cfg.cac, isinglink.derive_seed(cfg.seed, _DOM_BENCH, i))
+                   for i, inst in enumerate(instances)]
+            timings[name] = (time.perf_counter() - t0) / len(instances)
+            outputs[name] = np.array([r.x_hard for r in res])
+    H = np.array([inst.H for inst in instances])
+    y = np.array([inst.y for inst in instances])
+    nv = np.array([inst.noise_var for inst in instances], dtype=np.float64)
+    seeds = _seeds([[cfg.seed, _DOM_BENCH, i] for i in range(len(instances))])
+    const = instances[0].constellation
+    for prec in ("fp64_exact", "fp32"):
+        prm = dataclasses.replace(_params(cfg), precision=prec)
+        batched.detect_cim_batch(H, y, nv, len(const.points), seeds, prm)  # warm
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = batched.detect_cim_batch(H, y, nv, len(const.points), seeds, prm)
+        torch.cuda.synchronize()
+        timings[f"cuda_batched_{prec}"] = (time.perf_counter() - t0) / len(instances)
+        lv = torch.as_tensor(const.pam_levels)
+        idx = r.x_idx.cpu().long()
+        outputs[f"cuda_batched_{prec}"] = (lv[idx[..., 0]] + 1j * lv[idx[..., 1]]).numpy()
+    ref = outputs["ext"]
+    return {
+        "per_instance_s": timings,
+        "speedup_vs_ext": {k: timings["ext"] / v for k, v in timings.items()},
+        "output_agreement_with_ext": {k: float(np.mean(np.all(v == ref, axis=1)))
+                                      for k, v in outputs.items()},
+        "n_probe": len(instances),
+    }
+
+
 def run_bench(cfg, precisions=("fp32", "tf32", "fp64_exact"), chunks=(1, 4)) -> dict:
     """Throughput report over a fixed detection batch (bench.py:147-203).
 

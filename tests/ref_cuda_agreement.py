@@ -171,3 +171,29 @@ print("fork-before-init ok", rows[0].ser)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "fork-before-init ok" in r.stdout
+
+
+def test_kernel_comparison_row_with_cuda():
+    """The reference's _kernel_comparison (harness/bench.py:117-144) with
+    "cuda" among the kernels: per-instance detect_cim time of
+    every backend through the reference's code path, plus the batched slot
+    path, and decision agreement with "ext"."""
+    import json
+    import dataclasses as dc
+    import isinglink
+    from isinglink.harness import ExperimentConfig
+    from paper_2510_01579_b200 import harness
+    cfg = dc.replace(ExperimentConfig(), mode="bench", n_r=8, n_t=8, modulation=16,
+                     snr_grid_db=(20.0,), batch_size=64, seed=1)
+    row = harness.kernel_comparison(isinglink, cfg, n_probe=64)
+    print(json.dumps(row, indent=1))
+    out = os.environ.get("ISINGLINK_KCMP_OUT")
+    if out:
+        out = out if os.path.isabs(out) else os.path.join(ROOT, out)
+        with open(out, "w") as fh:
+            json.dump(row, fh, indent=1)
+    agree = row["output_agreement_with_ext"]
+    assert agree["cuda"] == 1.0
+    assert agree["cuda_batched_fp64_exact"] == 1.0
+    assert agree["cuda_batched_fp32"] >= 0.95
+    assert agree["python"] >= 0.95  # the reference's own allowance (test_backends.py)
