@@ -439,7 +439,10 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
         }
     }
     __syncwarp();
-    mbar_wait(bar, 0);
+    // with precomputed energies the selection needs H, y only for the decoded
+    // residual: the argmin runs while the bulk copies are in flight
+    const double e_guess_pre = energy[prob], off_pre = offset[prob];
+    if (!energies) mbar_wait(bar, 0);
     double gsum = 0.0;
     if (!energies)
         for (int i = 0; i < N; ++i) gsum += G[i * N + i];
@@ -490,15 +493,16 @@ __global__ void k_select_decode(const double* __restrict__ Hg, const double* __r
     ndiv = __reduce_add_sync(kFull, ndiv);
     if (diverged_count && lane == 0) diverged_count[prob] = ndiv;
     if (!(best_e < INFINITY)) best_i = -1;
+    if (energies) mbar_wait(bar, 0);
 
     uint8_t* idx = x_idx + prob * 2 * n_t;
-    const double e_guess = energy[prob];
+    const double e_guess = e_guess_pre;
     bool take = false;
     double e_dec = 0.0;
     __shared__ uint8_t cand_all[8][128];
     __shared__ cplx xs_all[8][64];
     uint8_t* cand = cand_all[warp];
-    if (best_i >= 0 && !(best_e + offset[prob] > e_guess)) {
+    if (best_i >= 0 && !(best_e + off_pre > e_guess)) {
         const int8_t* s = sp0 + (int64_t)best_i * S;
         const int aux = s[2 * N];
         for (int k = lane; k < N; k += 32) {
