@@ -103,7 +103,9 @@ def test_packed_vpp_equals_padded():
                       lv[torch.randint(0, 4, (P, n), device="cuda", generator=g)])
     tau = float(2.0 * (lv[-1] + (lv[1] - lv[0]) / 2))
     seeds = torch.arange(P, dtype=torch.int64, device="cuda")
-    prm = CacParams(n_anneals=8, precision="fp32")
-    a, b = _both(lambda: batched.precode_vpp_batch(H, u, float(n), tau, seeds, prm))
-    assert torch.equal(a.v, b.v)
-    assert np.array_equal(a.unnormalized_power.cpu().numpy(), b.unnormalized_power.cpu().numpy())
+    for stages, rng in ((1, "numpy"), (2, "numpy"), (2, "philox")):
+        prm = CacParams(n_anneals=8, precision="fp32", rng=rng)
+        a, b = _both(lambda: batched.precode_vpp_batch(H, u, float(n), tau, seeds, prm, n_stages=stages))
+        assert torch.equal(a.v, b.v), (stages, rng)
+        assert np.array_equal(a.unnormalized_power.cpu().numpy(), b.unnormalized_power.cpu().numpy())
+        assert torch.equal(a.diverged, b.diverged)
