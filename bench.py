@@ -229,7 +229,7 @@ def run_reference(args) -> None:
 
 def anneal_traffic():
     """DRAM bytes per k_anneal_fast launch from the committed ncu capture."""
-    path = os.path.join(ROOT, "profiles", "r01_anneal_traffic.json")
+    path = os.path.join(ROOT, "profiles", "r02_anneal_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
