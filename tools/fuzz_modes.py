@@ -18,7 +18,7 @@ from paper_2510_01579_b200.params import CacParams  # noqa: E402
 
 def main():
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 40
-    rnd = random.Random(7)
+    rnd = random.Random(int(os.environ.get("FUZZ_SEED", "7")))
     dev = torch.device("cuda", 0)
     bad = 0
     for case in range(n):
