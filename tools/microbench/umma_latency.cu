@@ -1,0 +1,159 @@
+// Round-trip latency of the tcgen05 coupling refresh as anneal_umma.cu issues
+// it, against the legacy mma.sync chain of k_anneal_fast (dev tool).
+//
+// One CTA per SM, 4 warps.  Per iteration:
+//   umma:  every thread stores its A slice (4 x 16 B), fence.proxy.async,
+//          bar.sync, thread 0 issues `passes` x KT tcgen05.mma (M = 64,
+//          N = 64, K = 16, f16 -> f32) + commit; all wait on the mbarrier,
+//          then tcgen05.ld 16x256b x NT and wait::ld;
+//   hmma:  each warp issues the same work as mma.sync.m16n8k16 (3 x 2 x 4).
+// Prints cycles per iteration (clock64, one warp's view), i.e. the latency a
+// warp waits per refresh when nothing else hides it.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o umma_latency umma_latency.cu && ./umma_latency
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#define ITERS 256
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint64_t smem_desc(const void* p, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = (uint64_t)((smem_u32(p) & 0x3FFFFu) >> 4);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
+    return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+template <int PASSES>
+__global__ void __launch_bounds__(128, 1) k_umma(long long* out) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tslot;
+    uint8_t* A = sm;          // 64 rows x 32 K f16 (4 KB), hi
+    uint8_t* B = sm + 8192;   // 32 K x 64 cols f16 (4 KB)
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 16384 / 4; i += 128) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u * (i & 1);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tslot)), "r"(64)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (threadIdx.x == 32) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = tslot;
+    const uint64_t ad = smem_desc(A, 8 * 128, 128), bd = smem_desc(B, 8 * 16, 128);
+    uint32_t phase = 0;
+    float acc = 0.f;
+    long long t0 = 0;
+    for (int it = -8; it < ITERS; ++it) {
+        if (it == 0) t0 = clock64();
+        // A operand rows of this thread (4 x 16 B), as the kernel writes them
+        for (int q = 0; q < 4; ++q)
+            reinterpret_cast<uint4*>(A)[(threadIdx.x * 4 + q) & 255] = make_uint4(it, q, 0, 0);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int p = 0; p < PASSES; ++p)
+                for (int kt = 0; kt < 2; ++kt) {
+                    const uint32_t accf = (p | kt) ? 1u : 0u;
+                    asm volatile(
+                        "{\n .reg .pred pp;\n setp.ne.b32 pp, %4, 0;\n"
+                        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, pp;\n}\n" ::"r"(tmem),
+                        "l"(ad + (uint64_t)((2 * kt * 8 * 128) >> 4)), "l"(bd + (uint64_t)((2 * kt * 64 * 16) >> 4)),
+                        "r"(idesc_f16(64, 64)), "r"(accf)
+                        : "memory");
+                }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             smem_u32(&bar))
+                         : "memory");
+        }
+        uint32_t done = 0, spins = 0;
+        while (!done) {
+            if (++spins > (1u << 24)) __trap();  // watchdog: a lost arrive traps instead of hanging
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(smem_u32(&bar)), "r"(phase)
+                : "memory");
+        }
+        phase ^= 1u;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float r[4][4];
+        for (int n = 0; n < 4; ++n)
+            asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(r[n][0]), "=f"(r[n][1]), "=f"(r[n][2]), "=f"(r[n][3])
+                         : "r"(tmem + ((uint32_t)(32 * warp) << 16) + 8 * n)
+                         : "memory");
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        acc += r[0][0] + r[3][3];
+    }
+    const long long t1 = clock64();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64) : "memory");
+    if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / ITERS;
+    if (acc == 1234.5f) out[0] = 0;
+}
+
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int PASSES>
+__global__ void __launch_bounds__(128, 1) k_hmma(long long* out) {
+    uint32_t a[4] = {threadIdx.x, 1u, 2u, 3u}, b0 = 0x3c003c00u, b1 = threadIdx.x;
+    float acc[4][4] = {};
+    long long t0 = 0;
+    for (int it = -8; it < ITERS; ++it) {
+        if (it == 0) t0 = clock64();
+        float d[4][4] = {};
+        for (int p = 0; p < PASSES; ++p)
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                for (int n = 0; n < 4; ++n) mma_f16(d[n], a, b0 + kt + p, b1 + n);
+#pragma unroll
+        for (int n = 0; n < 4; ++n) acc[n][0] += d[n][0];  // the refresh result is consumed
+        a[0] = __float_as_uint(acc[0][0]);
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) out[blockIdx.x] = (t1 - t0) / ITERS;
+    if (acc[1][0] == 1234.5f) out[1] = 0;
+}
+
+int main() {
+    long long* d;
+    cudaMalloc(&d, 8 * 148);
+    long long h[148];
+    auto run = [&](const char* name, void (*k)(long long*), size_t smem) {
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k<<<148, 128, smem>>>(d);
+        cudaError_t e = cudaDeviceSynchronize();
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        long long s = 0;
+        for (int i = 0; i < 148; ++i) s += h[i];
+        printf("%-28s %6lld cycles per refresh (%s)\n", name, s / 148, cudaGetErrorString(e));
+    };
+    run("tcgen05 3 passes (fp32)", k_umma<3>, 16384);
+    run("tcgen05 2 passes (mixed)", k_umma<2>, 16384);
+    run("tcgen05 1 pass (tf32)", k_umma<1>, 16384);
+    run("mma.sync 3 passes (24 HMMA)", k_hmma<3>, 0);
+    run("mma.sync 1 pass (8 HMMA)", k_hmma<1>, 0);
+    return 0;
+}
