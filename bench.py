@@ -120,13 +120,32 @@ _CPU_CTX = {}
 
 def _cpu_worker(args):
     H, y, s2, seed = args
+    ref = _CPU_CTX.get("ref")
+    if ref is not None:  # the reference package's own detect_cim (detector.py:57-82)
+        inst = ref.MimoInstance(H=H, y=y, constellation=_CPU_CTX["const"], noise_var=float(s2))
+        return ref.detect_cim(inst, seed=int(seed)).energy
     orc = _CPU_CTX["orc"]
-    kernel = _CPU_CTX["kernel"]
-    r = orc.detect_cim(H, y, float(s2), ORDER, seed=int(seed), kernel=kernel)
+    r = orc.detect_cim(H, y, float(s2), ORDER, seed=int(seed), kernel=_CPU_CTX["kernel"])
     return r["energy"]
 
 
+REF_PKG = os.path.join(ROOT, "oracle", "_ref", "pkg")
+
+
 def _cpu_init():
+    """The reference's own package (staged by `make -C oracle refpkg`, its
+    compiled kernel as the "ext" backend) when present; else the oracle's
+    restatement around the reference kernel (or the C port)."""
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    if os.path.isdir(os.path.join(REF_PKG, "isinglink")):
+        if REF_PKG not in sys.path:
+            sys.path.insert(0, REF_PKG)
+        import isinglink
+        if isinglink.kernel_backend() == "ext":
+            _CPU_CTX["ref"] = isinglink
+            _CPU_CTX["const"] = isinglink.make_qam(ORDER)
+            return
     from oracle import isinglink_oracle as orc
     _CPU_CTX["orc"] = orc
     ref = orc.ref_kernel_module()
@@ -166,6 +185,16 @@ def cpu_rate(n_res: int, cores: int, pool=None):
 def cpu_kind() -> str:
     from oracle import isinglink_oracle as orc
     return "reference" if orc.ref_kernel_module() is not None else "port"
+
+
+def cpu_path() -> str:
+    """What the CPU legs run (see _cpu_init)."""
+    if os.path.isdir(os.path.join(REF_PKG, "isinglink")):
+        return ("the reference package's own detect_cim (oracle/_ref/pkg, unmodified sources) "
+                "with its compiled Cython kernel as the ext backend")
+    if cpu_kind() == "reference":
+        return "the reference Cython kernel (oracle/_ref) inside the oracle's detect_cim glue"
+    return "the C oracle kernel inside the oracle's detect_cim glue"
 
 
 def host_cores() -> int:
@@ -211,8 +240,7 @@ def run_reference(args) -> None:
     total = per_step * args.steps
     value = total / sum(times)
     sample = (f"{per_step} fresh 16x16 16-QAM 20 dB REs per step on {cores} host processes; "
-              + ("reference Cython kernel (oracle/_ref) inside the oracle's detect_cim glue"
-                 if kind == "reference" else "C oracle kernel inside the oracle's detect_cim glue"))
+              + cpu_path())
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
@@ -624,9 +652,7 @@ def run_ours(args) -> None:
         kind = cpu_kind()
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                "sample": f"{n_cpu} fresh 16x16 16-QAM 20 dB REs on {cores} host processes "
-                         f"({dt:.1f} s); " + ("reference Cython kernel (oracle/_ref)" if kind ==
-                                                "reference" else "C oracle kernel")
-                         + " inside the oracle's detect_cim"}
+                         f"({dt:.1f} s); " + cpu_path()}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
