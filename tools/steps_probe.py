@@ -14,12 +14,13 @@ P = 45864
 H, y, nv, seeds, _ = batch(16, 16, 20.0, P, 3)
 import os
 PREC = os.environ.get("PREC", "fp32")
-for steps, f in ((2, 2), (32, 2), (128, 2), (256, 2), (128, 1), (128, 4), (128, 128), (256, 256)):
-    prm = CacParams(f_mvm=f, n_steps=steps, precision=PREC)
+RNG = os.environ.get("RNG", "numpy")
+for steps, f in ((2, 2), (32, 2), (128, 2), (256, 2), (128, 1), (128, 4), (128, 128), (256, 256), (4, 2), (8, 2)):
+    prm = CacParams(f_mvm=f, n_steps=steps, precision=PREC, rng=RNG)
     batched.detect_cim_batch(H, y, nv, 16, seeds, prm)
     torch.cuda.synchronize()
     _lib.profile_begin()
     for _ in range(3):
         batched.detect_cim_batch(H, y, nv, 16, seeds, prm)
     pr = _lib.profile_end()
-    print(f"n_steps={steps} f_mvm={f}: anneal {pr['anneal'][0] / 3:.3f} ms", flush=True)
+    print(f"{PREC} {RNG} n_steps={steps} f_mvm={f}: anneal {pr['anneal'][0] / 3:.3f} ms", flush=True)
