@@ -30,7 +30,7 @@ __host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
     return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-template <int PASSES>
+template <int PASSES, bool FENCE = true, bool LD = true, bool STA = true, bool BAR = true>
 __global__ void __launch_bounds__(128, 1) k_umma(long long* out) {
     extern __shared__ __align__(128) uint8_t sm[];
     __shared__ uint64_t bar;
@@ -59,11 +59,13 @@ __global__ void __launch_bounds__(128, 1) k_umma(long long* out) {
     for (int it = -8; it < ITERS; ++it) {
         if (it == 0) t0 = clock64();
         // A operand rows of this thread (4 x 16 B), as the kernel writes them
-        for (int q = 0; q < 4; ++q)
-            reinterpret_cast<uint4*>(A)[(threadIdx.x * 4 + q) & 255] = make_uint4(it, q, 0, 0);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (STA)
+            for (int q = 0; q < 4; ++q)
+                reinterpret_cast<uint4*>(A)[(threadIdx.x * 4 + q) & 255] = make_uint4(it, q, 0, 0);
+        if (FENCE) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (BAR) asm volatile("bar.sync 1, 128;" ::: "memory");
+        else __syncwarp();
         if (threadIdx.x == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int p = 0; p < PASSES; ++p)
@@ -91,13 +93,15 @@ __global__ void __launch_bounds__(128, 1) k_umma(long long* out) {
         }
         phase ^= 1u;
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float r[4][4];
+        float r[4][4] = {};
+        if (LD) {
         for (int n = 0; n < 4; ++n)
             asm volatile("tcgen05.ld.sync.aligned.16x256b.x1.b32 {%0, %1, %2, %3}, [%4];"
                          : "=f"(r[n][0]), "=f"(r[n][1]), "=f"(r[n][2]), "=f"(r[n][3])
                          : "r"(tmem + ((uint32_t)(32 * warp) << 16) + 8 * n)
                          : "memory");
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        }
         acc += r[0][0] + r[3][3];
     }
     const long long t1 = clock64();
@@ -153,6 +157,12 @@ int main() {
     run("tcgen05 3 passes (fp32)", k_umma<3>, 16384);
     run("tcgen05 2 passes (mixed)", k_umma<2>, 16384);
     run("tcgen05 1 pass (tf32)", k_umma<1>, 16384);
+    run("3 passes, no proxy fence", k_umma<3, false>, 16384);
+    run("3 passes, no tcgen05.ld", k_umma<3, true, false>, 16384);
+    run("3 passes, no A stores", k_umma<3, true, true, false>, 16384);
+    run("3 passes, no A stores/fence", k_umma<3, false, true, false>, 16384);
+    run("0 MMAs (commit only)", k_umma<0>, 16384);
+    run("0 MMAs, no fence, no ld", k_umma<0, false, false>, 16384);
     run("mma.sync 3 passes (24 HMMA)", k_hmma<3>, 0);
     run("mma.sync 1 pass (8 HMMA)", k_hmma<1>, 0);
     return 0;
