@@ -22,6 +22,9 @@
 //                                  polynomial of the (power-of-two scaled) T.
 // One Gram per RE: its rows are written as G, then eliminated in place by
 // the MMSE; lambda_max needs no copy of them (no global scratch).
+#ifndef IL_FRONT_CPASYNC  // H, y staged by cp.async (0: through registers, 0.555 vs 0.540 ms)
+#define IL_FRONT_CPASYNC 1
+#endif
 #include <float.h>
 
 #include "il_group.cuh"
@@ -245,8 +248,22 @@ __device__ __forceinline__ void front_group(const Grp<GS>& g, int64_t prob, cplx
     {
         const cplx* Hp = reinterpret_cast<const cplx*>(Hg) + prob * (int64_t)n_r * n;
         const cplx* yp = reinterpret_cast<const cplx*>(yg) + prob * (int64_t)n_r;
+#if IL_FRONT_CPASYNC
+        // asynchronous 16-byte copies straight into shared memory: all of a
+        // lane's loads in flight at once, no register staging
+        for (int i = r; i < n_r * n; i += GS)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(H + i)),
+                         "l"(Hp + i)
+                         : "memory");
+        for (int i = r; i < n_r; i += GS)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(y + i)),
+                         "l"(yp + i)
+                         : "memory");
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#else
         for (int i = r; i < n_r * n; i += GS) H[i] = Hp[i];
         for (int i = r; i < n_r; i += GS) y[i] = yp[i];
+#endif
     }
     g.sync();
     const double c = 0.5 * al.spacing;
