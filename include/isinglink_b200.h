@@ -9,7 +9,9 @@
  *     others take DEVICE pointers and enqueue on `stream` (a cudaStream_t,
  *     NULL = legacy default stream) without synchronising;
  *   - complex arrays are interleaved (re, im) float64, i.e. numpy complex128
- *     / torch.complex128 memory;
+ *     / torch.complex128 memory; the detection entries stage H and y with
+ *     16-byte asynchronous copies and require them 16-byte aligned (every
+ *     CUDA allocation and every complex128 element of one is), else IL_ERR_ARG;
  *   - return 0 (IL_OK) on success, a negative IL_ERR_* code otherwise, with a
  *     human-readable message from il_last_error() (thread-local).  No C++
  *     exception ever crosses the ABI.  Divergence of an anneal is data, not

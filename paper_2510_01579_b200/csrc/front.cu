@@ -807,6 +807,9 @@ int launch_select_decode(const double* H, const double* y, const double* G, cons
     if (P == 0) return IL_OK;
     const int N = 2 * n_t;
     IL_REQUIRE(2 * n_t <= 128, "n_t too large");
+    // H, y (and G, b) arrive by 1-D bulk copies: 16-byte aligned sources
+    IL_REQUIRE((((uintptr_t)H | (uintptr_t)y | (uintptr_t)G | (uintptr_t)b) & 15u) == 0,
+               "H and y must be 16-byte aligned (complex128 device arrays)");
     const size_t per_warp = sel_warp_bytes(n_r, n_t, energies == nullptr);
     int wpb = (int)((200 * 1024) / per_warp);
     wpb = wpb < 1 ? 1 : (wpb > 8 ? 8 : wpb);

@@ -505,6 +505,9 @@ int launch_front_rows(bool do_mmse, bool do_ising, const double* H, const double
                       uint8_t* x_idx, double* energy, int8_t* status, const IsingOut& o,
                       cudaStream_t st) {
     if (P == 0) return IL_OK;
+    // H and y are staged by 16-byte cp.async copies
+    IL_REQUIRE((((uintptr_t)H | (uintptr_t)y) & 15u) == 0,
+               "H and y must be 16-byte aligned (complex128 device arrays)");
 #define IL_ROWS(GS)                                                                                \
     do {                                                                                           \
         if (do_mmse && do_ising)                                                                   \

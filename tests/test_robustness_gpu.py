@@ -99,3 +99,26 @@ def test_concurrent_calls_from_threads_match_serial():
     assert not errs, errs
     for k in range(4):
         assert torch.equal(got[k], want[k % 2])
+
+
+def test_misaligned_h_y_rejected():
+    """The detection front end stages H and y with 16-byte copies: a pointer
+    that is only 8-byte aligned is an IL_ERR_ARG (ValueError), not a fault."""
+    from paper_2510_01579_b200 import _lib, batched
+    d = load_golden("d8x8_16qam_20db.npz")
+    P, n_r, n_t = 4, 8, 8
+    H = torch.as_tensor(d["H"][:P]).cuda()
+    y = torch.as_tensor(d["y"][:P]).cuda()
+    s2 = torch.full((P,), 0.08, dtype=torch.float64, device="cuda")
+    # the same values behind an address offset by one float64
+    Hf = torch.empty(P * n_r * n_t * 2 + 1, dtype=torch.float64, device="cuda")
+    Hf[1:] = torch.view_as_real(H).reshape(-1)
+    x_idx = torch.empty((P, n_t, 2), dtype=torch.uint8, device="cuda")
+    energy = torch.empty(P, dtype=torch.float64, device="cuda")
+    status = torch.empty(P, dtype=torch.int8, device="cuda")
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        _lib.call("il_mmse_batch", Hf.data_ptr() + 8, y.data_ptr(), s2.data_ptr(), P, n_r, n_t, 16,
+                  x_idx.data_ptr(), energy.data_ptr(), status.data_ptr(), None)
+    # the aligned call still works afterwards
+    xi, en, st = batched.mmse_batch(H, y, s2, 16)
+    assert torch.isfinite(en).all()
