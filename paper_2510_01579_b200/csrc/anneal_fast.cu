@@ -13,7 +13,7 @@ using namespace fastk;
 namespace {
 // Register layouts built: N = 8 NT spins per half for these NT; a problem of
 // n spins runs on the smallest N >= n (inert padding spins, see k_anneal_fast).
-constexpr int kFastNT[] = {1, 2, 3, 4, 6, 8};
+constexpr int kFastNT[] = {1, 2, 3, 4, 5, 6, 7, 8};
 int fast_nt_for(int n) {
     for (int nt : kFastNT)
         if (8 * nt >= n) return nt;
@@ -130,7 +130,9 @@ int launch_anneal_fast(const double* G, const double* g, const double* b,
         IL_NT(2);
         IL_NT(3);
         IL_NT(4);
+        IL_NT(5);
         IL_NT(6);
+        IL_NT(7);
         IL_NT(8);
 #undef IL_NT
         default:

@@ -971,7 +971,9 @@ IL_FAST_NT_DECL(1);
 IL_FAST_NT_DECL(2);
 IL_FAST_NT_DECL(3);
 IL_FAST_NT_DECL(4);
+IL_FAST_NT_DECL(5);
 IL_FAST_NT_DECL(6);
+IL_FAST_NT_DECL(7);
 IL_FAST_NT_DECL(8);
 
 }  // namespace il
