@@ -15,6 +15,8 @@
 //   vpp post        precoder.py:126-146
 #include <float.h>
 
+#include <algorithm>
+
 #include "il_internal.cuh"
 #include "rng_numpy.cuh"
 
@@ -252,17 +254,16 @@ __device__ double lambda_max_hermitian(cplx* A, int n, cplx* scratch, int lane) 
 
 // Per-warp shared-memory carve-up for the detection front-end.
 struct FrontSmem {
-    cplx *H, *y, *A, *M, *z, *r, *scr;
+    cplx *H, *y, *A, *z, *r, *scr;
     IL_HD static size_t bytes(int n_r, int n_t) {
-        const size_t c = (size_t)n_r * n_t + n_r + 2 * (size_t)n_t * n_t + n_t + n_r + 5 * n_t + 4;
+        const size_t c = (size_t)n_r * n_t + n_r + (size_t)n_t * n_t + n_t + n_r + 5 * n_t + 4;
         return c * sizeof(cplx);
     }
     __device__ void carve(char* base, int n_r, int n_t) {
         H = reinterpret_cast<cplx*>(base);
         y = H + n_r * n_t;
         A = y + n_r;
-        M = A + n_t * n_t;
-        z = M + n_t * n_t;
+        z = A + n_t * n_t;
         r = z + n_t;
         scr = r + n_r;
     }
@@ -292,9 +293,10 @@ __device__ double residual_from_idx(const cplx* H, const cplx* y, const uint8_t*
     return warp_sum(acc);
 }
 
-// G, g_diag, b, offset, eps_scale around the guess whose residual is r (r2 = ||r||^2).
-__device__ void emit_ising(cplx* H, const cplx* r, double r2, cplx* A, cplx* scr, int n_r, int n_t,
-                           const Alphabet& al, int64_t prob, const IsingOut& o, int lane) {
+// G and g_diag from the Gram matrix A (transform.py:108-140); returns tr(G)
+// on every lane.
+__device__ double emit_g(const cplx* A, int n_t, const Alphabet& al, int64_t prob,
+                         const IsingOut& o, int lane) {
     const int N = 2 * n_t;
     const double c = 0.5 * al.spacing;
     const double c2 = c * c;
@@ -315,6 +317,20 @@ __device__ void emit_ising(cplx* H, const cplx* r, double r2, cplx* A, cplx* scr
             o.g[prob * N + n_t + i] = gi;
         }
         tr += 2.0 * gi;
+    }
+    return warp_sum(tr);
+}
+
+// b, offset and eps_scale around the guess whose residual is r (r2 =
+// ||r||^2); lambda_max is taken of c^2 A as stored in G (its blocks [[Re,
+// -Im], [Im, Re]] read back into the shared-memory slot W, so that A itself
+// may have been factorised in place by then).
+__device__ void emit_rest(const cplx* H, const cplx* r, double r2, double trg, cplx* W, cplx* scr,
+                          int n_r, int n_t, const Alphabet& al, int64_t prob, const IsingOut& o,
+                          int lane) {
+    const int N = 2 * n_t;
+    const double c = 0.5 * al.spacing;
+    for (int i = lane; i < n_t; i += 32) {
         // H^H r
         double re = 0.0, im = 0.0;
         for (int k = 0; k < n_r; ++k) {
@@ -325,12 +341,16 @@ __device__ void emit_ising(cplx* H, const cplx* r, double r2, cplx* A, cplx* scr
         o.b[prob * N + i] = -c * re;
         o.b[prob * N + n_t + i] = -c * im;
     }
-    tr = warp_sum(tr);
+    const double* G = o.G + prob * (int64_t)N * N;
+    __syncwarp();  // this warp's G stores are visible to its loads
+    for (int idx = lane; idx < n_t * n_t; idx += 32) {
+        const int i = idx / n_t, j = idx % n_t;
+        W[idx] = {G[i * N + j], G[(n_t + i) * N + j]};
+    }
     __syncwarp();
-    const double lam_a = lambda_max_hermitian(A, n_t, scr, lane);
+    const double lam = lambda_max_hermitian(W, n_t, scr, lane);
     if (lane == 0) {
-        if (o.offset) o.offset[prob] = r2 + 2.0 * tr;
-        const double lam = c2 * lam_a;
+        if (o.offset) o.offset[prob] = r2 + 2.0 * trg;  // ||r||^2 + 2 tr G
         const double S = (double)(2 * N + 1);
         const double es = 32.0 / sqrt(fmax(lam, 1e-30) * S);
         if (o.eps_scale) o.eps_scale[prob] = es;
@@ -355,19 +375,19 @@ __global__ void k_front(const double* __restrict__ Hg, const double* __restrict_
     load_problem(Hg, yg, prob, n_r, n_t, sm.H, sm.y, lane);
     gram_hermitian(sm.H, sm.y, n_r, n_t, sm.A, sm.z, lane);
     uint8_t* idx = x_idx + prob * 2 * n_t;
+    // G first, so that the MMSE may factorise A in place (no second n_t^2 slot:
+    // more warps per SM for these large shapes)
+    const double trg = DO_ISING ? emit_g(sm.A, n_t, al, prob, o, lane) : 0.0;
+    __syncwarp();  // every lane's reads of A precede the in-place factorisation
     if (DO_MMSE) {
         const double s2 = s2g[prob];
-        for (int i = lane; i < n_t * n_t; i += 32) {
-            cplx a = sm.A[i];
-            if (i / n_t == i % n_t) a.re += s2;
-            sm.M[i] = a;
-        }
+        for (int i = lane; i < n_t; i += 32) sm.A[i * n_t + i].re += s2;
         __syncwarp();
         double* invd = reinterpret_cast<double*>(sm.scr);
-        const bool ok = cholesky_lower(sm.M, n_t, invd, lane);
+        const bool ok = cholesky_lower(sm.A, n_t, invd, lane);
         if (status && lane == 0) status[prob] = ok ? 0 : -1;
         if (ok) {
-            cholesky_solve(sm.M, invd, n_t, sm.z, lane);
+            cholesky_solve(sm.A, invd, n_t, sm.z, lane);
             for (int j = lane; j < n_t; j += 32) {
                 idx[2 * j] = (uint8_t)level_index(sm.z[j].re, al);
                 idx[2 * j + 1] = (uint8_t)level_index(sm.z[j].im, al);
@@ -379,12 +399,24 @@ __global__ void k_front(const double* __restrict__ Hg, const double* __restrict_
     }
     const double r2 = residual_from_idx(sm.H, sm.y, idx, n_r, n_t, al, sm.r, sm.scr, lane);
     if (energy && lane == 0) energy[prob] = r2;
-    if (DO_ISING) emit_ising(sm.H, sm.r, r2, sm.A, sm.scr, n_r, n_t, al, prob, o, lane);
+    if (DO_ISING) emit_rest(sm.H, sm.r, r2, trg, sm.A, sm.scr, n_r, n_t, al, prob, o, lane);
 }
 
 int front_blocks(int64_t P, size_t per_warp, int* wpb, size_t* smem) {
-    int w = (int)((200 * 1024) / per_warp);
-    w = w < 1 ? 1 : (w > 4 ? 4 : w);
+    // warps per CTA (4, 2 or 1) that fit the most warps per SM into its
+    // 227 KB of shared memory (1 KB reserved per CTA): for n_t = 28, 1-warp
+    // CTAs hold 7 warps per SM where 4-warp CTAs held 4
+    const size_t sm_bytes = 227 * 1024;
+    int w = 1, best = 0;
+    for (int c : {4, 2, 1}) {
+        if (c * per_warp > 200 * 1024) continue;
+        const int ctas = (int)(sm_bytes / (c * per_warp + 1024));
+        const int warps = std::min(ctas * c, 48);
+        if (warps > best) {
+            best = warps;
+            w = c;
+        }
+    }
     *wpb = w;
     *smem = per_warp * w;
     return (int)((P + w - 1) / w);

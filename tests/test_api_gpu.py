@@ -131,6 +131,24 @@ class TestIsing:
             assert si.offset == pytest.approx(o["offset"], rel=1e-12)
             assert si.eps_scale == pytest.approx(o["eps_scale"], rel=1e-12)
 
+    def test_large_shapes_match_oracle(self):
+        """16 < n_t <= 32 take the warp-per-RE front end (k_front): MMSE
+        decisions, residual and the Ising coefficients against the oracle."""
+        for n_r, n_t, order in ((20, 20, 16), (30, 28, 4), (32, 32, 16)):
+            for trial in range(2):
+                inst = random_instance(n_r, n_t, order, 20.0, tag=2100 + n_t, trial=trial)
+                lv = inst.constellation.pam_levels
+                mm = api.detect_mmse(inst)
+                xh, e = orc.mmse(inst.H, inst.y, inst.noise_var, lv)
+                np.testing.assert_array_equal(mm.x_hard, xh)
+                assert mm.energy == pytest.approx(e, rel=1e-12)
+                si = api.build_ising(inst, mm.x_hard)
+                o = orc.ising(inst.H, inst.y, mm.x_hard, inst.constellation.spacing)
+                np.testing.assert_allclose(si.G, o["G"], rtol=1e-12, atol=1e-13)
+                np.testing.assert_allclose(si.b, o["b"], rtol=1e-12, atol=1e-12)
+                assert si.offset == pytest.approx(o["offset"], rel=1e-12)
+                assert si.eps_scale == pytest.approx(o["eps_scale"], rel=1e-12)
+
 
 # ------------------------------------------------------------------- solver --
 class TestSolver:
