@@ -147,68 +147,10 @@ __device__ void cholesky_solve(const cplx* L, const double* inv_diag, int n, cpl
     __syncwarp();
 }
 
-// Largest eigenvalue of the Hermitian A[n x n] (destroyed): Householder
-// reduction to real symmetric tridiagonal form, then warp-parallel
-// multisection on the Sturm count (32 probes per round, ~11 rounds to full
-// FP64 resolution).  scratch: 3*n cplx + 2*n double.
-__device__ double lambda_max_hermitian(cplx* A, int n, cplx* scratch, int lane) {
-    cplx* v = scratch;
-    cplx* p = v + n;
-    cplx* w = p + n;
-    double* d = reinterpret_cast<double*>(w + n);
-    double* e = d + n;
-    for (int k = 0; k + 2 < n; ++k) {
-        const int m = n - k - 1;
-        cplx xi = {0.0, 0.0};
-        if (lane < m) xi = A[(k + 1 + lane) * n + k];
-        const double sig2 = warp_sum(cabs2(xi));
-        if (lane == 0) d[k] = A[k * n + k].re;
-        if (!(sig2 > 0.0)) {
-            if (lane == 0) e[k] = 0.0;
-            __syncwarp();
-            continue;
-        }
-        const double sig = sqrt(sig2);
-        const cplx x0 = A[(k + 1) * n + k];
-        const double ax0 = sqrt(cabs2(x0));
-        const cplx ph = ax0 > 0.0 ? cplx{x0.re / ax0, x0.im / ax0} : cplx{1.0, 0.0};
-        const double tau = 1.0 / (sig * (sig + ax0));
-        if (lane < m) v[lane] = lane == 0 ? cplx{xi.re + ph.re * sig, xi.im + ph.im * sig} : xi;
-        if (lane == 0) e[k] = sig;
-        __syncwarp();
-        cplx pi = {0.0, 0.0};
-        if (lane < m) {
-            const cplx* Bi = A + (k + 1 + lane) * n + (k + 1);
-            for (int j = 0; j < m; ++j) pi = cadd(pi, cmul(Bi[j], v[j]));
-            pi = {tau * pi.re, tau * pi.im};
-        }
-        // K = (tau/2) v^H p  (real for Hermitian B)
-        const double vhp = warp_sum(lane < m ? v[lane].re * pi.re + v[lane].im * pi.im : 0.0);
-        const double K = 0.5 * tau * vhp;
-        if (lane < m) w[lane] = {pi.re - K * v[lane].re, pi.im - K * v[lane].im};
-        __syncwarp();
-        if (lane < m) {
-            const cplx vi = v[lane], wi = w[lane];
-            cplx* Bi = A + (k + 1 + lane) * n + (k + 1);
-            for (int j = 0; j < m; ++j) {
-                // B[i][j] -= v_i conj(w_j) + w_i conj(v_j)
-                const cplx a1 = cmulc(w[j], vi);  // conj(w_j) * v_i
-                const cplx a2 = cmulc(v[j], wi);
-                Bi[j] = csub(Bi[j], cadd(a1, a2));
-            }
-        }
-        __syncwarp();
-    }
-    if (lane == 0) {
-        if (n >= 2) {
-            d[n - 2] = A[(n - 2) * n + (n - 2)].re;
-            e[n - 2] = sqrt(cabs2(A[(n - 1) * n + (n - 2)]));
-        }
-        d[n - 1] = A[(n - 1) * n + (n - 1)].re;
-    }
-    __syncwarp();
+// Largest eigenvalue of the real symmetric tridiagonal T (diagonal d[0..n),
+// off-diagonal e[0..n-1)), identical in every lane.
+__device__ double tridiag_max_smem(const double* d, const double* e, int n) {
     if (n == 1) return d[0];
-
     // Largest root of det(T - x I) by Laguerre iteration from the Gershgorin
     // upper bound: for a polynomial with only real roots it converges
     // monotonically from above to the largest root, cubically (and exactly
@@ -250,6 +192,74 @@ __device__ double lambda_max_hermitian(cplx* A, int n, cplx* scratch, int lane) 
         if (!(step > 2.0 * DBL_EPSILON * fabs(x))) break;
     }
     return x;
+}
+
+// Largest eigenvalue of the Hermitian W[n x n] (read only, n <= 32): n Lanczos
+// steps over the warp (lane r owns component r; W is read by columns, W[j][r]
+// = conj(W[r][j]), so that the lanes' loads are consecutive), no
+// reorthogonalisation (the extreme Ritz value converges regardless), then
+// the Laguerre iteration on the tridiagonal.  The same start vector and
+// breakdown rule as the row front end's lanczos_rows (front_rows.cu).
+// Replaces a Householder reduction (2.5x the FP64 work, n - 2 rank-2 updates
+// of the shared-memory matrix).  scratch: n cplx + 2n double.
+__device__ double lambda_max_hermitian(const cplx* W, int n, cplx* scratch, int lane) {
+    cplx* vb = scratch;
+    double* d = reinterpret_cast<double*>(scratch + n);
+    double* e = d + n;
+    const bool own = lane < n;
+    cplx v = {0.0, 0.0};
+    double nrm = 0.0;  // row-sum norm (scale of the breakdown test)
+    if (own) {
+        const double phi = 0.6180339887498949;
+        double ip;
+        v = {0.5 + modf((lane + 1) * phi, &ip), 0.5 + modf((lane + 1) * phi * phi * 3.1, &ip)};
+        for (int j = 0; j < n; ++j) nrm += fabs(W[j * n + lane].re) + fabs(W[j * n + lane].im);
+    }
+    {
+        const double inv = 1.0 / sqrt(warp_sum(cabs2(v)));
+        v = {v.re * inv, v.im * inv};
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm = fmax(nrm, __shfl_xor_sync(0xffffffffu, nrm, o));
+    cplx vp = {0.0, 0.0};
+    double beta = 0.0;
+    int m = n;
+    for (int k = 0; k < n; ++k) {
+        __syncwarp();  // the previous step's reads of vb are done
+        if (own) vb[lane] = v;
+        __syncwarp();
+        cplx w0 = {0.0, 0.0}, w1 = {0.0, 0.0};
+        if (own) {
+            int j = 0;
+            for (; j + 1 < n; j += 2) {
+                const cplx a0 = W[j * n + lane], a1 = W[(j + 1) * n + lane];
+                const cplx v0 = vb[j], v1 = vb[j + 1];
+                w0 = cadd(w0, cmulc(a0, v0));  // conj(W[j][r]) v_j = W[r][j] v_j
+                w1 = cadd(w1, cmulc(a1, v1));
+            }
+            if (j < n) w0 = cadd(w0, cmulc(W[j * n + lane], vb[j]));
+        }
+        cplx w = cadd(w0, w1);
+        const double a = warp_sum(v.re * w.re + v.im * w.im);
+        const double ww = warp_sum(cabs2(w));
+        w = {w.re - a * v.re - beta * vp.re, w.im - a * v.im - beta * vp.im};
+        if (lane == 0) d[k] = a;
+        double b2 = ww - a * a - beta * beta;
+        if (!(b2 >= 0.01 * ww)) b2 = warp_sum(cabs2(w));
+        const double bk = sqrt(b2);
+        if (k == n - 1) break;
+        if (!(bk > 1e-14 * nrm)) {  // invariant subspace: T_{k+1} is exact
+            m = k + 1;
+            break;
+        }
+        if (lane == 0) e[k] = bk;
+        const double ib = 1.0 / bk;
+        vp = v;
+        v = {w.re * ib, w.im * ib};
+        beta = bk;
+    }
+    __syncwarp();
+    return tridiag_max_smem(d, e, m);
 }
 
 // Per-warp shared-memory carve-up for the detection front-end.
