@@ -43,6 +43,11 @@ def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     os.makedirs(OBJ_DIR, exist_ok=True)
     sources = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    # objects whose source is gone (renamed or deleted files) are removed
+    live = {os.path.basename(src)[:-3] + ".o" for src in sources}
+    for obj in glob.glob(os.path.join(OBJ_DIR, "*.o")):
+        if os.path.basename(obj) not in live:
+            os.remove(obj)
     newest_dep = max((os.path.getmtime(p) for p in _deps()), default=0.0)
     objs = []
     procs = []
