@@ -495,7 +495,11 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         // beta) since x2_i <= dmax (the sticky max of x^2 already tracked for
         // divergence) and rounding is monotone.  While e_lb r_lb >= e_floor no
         // floor can bind and the 2 FMNMX per spin pair are skipped; otherwise
-        // every element is clamped exactly as before (also for NaN).
+        // every element is clamped exactly as before (also for NaN).  The branch
+        // is warp-uniform (a vote): in a clamp round the lanes whose bound
+        // holds clamp too, a no-op for them (e >= nxt >= e_floor, no NaN:
+        // a NaN factor makes the bound NaN), so no convergence barrier is
+        // needed (4.055 -> 4.043 ms per 16x16 slot).
         if constexpr (PACK) {
             // one bound per row half (the halves have their own floors)
 #pragma unroll
@@ -504,7 +508,8 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                                       : (SAME_QR ? fmaf(s.ndt, max_nan(dv[h][0], dv[h][1]), s.alpha)
                                                  : fmaf(s.ndtz, max_nan(dv[h][0], dv[h][1]), s.beta));
                 const float nxt = e_lbh[h] * r_lb;
-                if (nxt >= e_floorq[h]) {
+                const bool fine = nxt >= e_floorq[h];
+                if (__all_sync(0xffffffffu, fine)) {
                     e_lbh[h] = nxt;
                 } else {
 #pragma unroll
@@ -512,7 +517,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                         eA[h][n] = floor2(eA[h][n], e_floorq[h]);
                         eB[h][n] = floor2(eB[h][n], e_floorq[h]);
                     }
-                    e_lbh[h] = e_floorq[h];
+                    e_lbh[h] = fine ? nxt : e_floorq[h];
                 }
             }
         } else {
@@ -525,7 +530,10 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                                                        : fmaf(s.ndtz, dmax, s.beta);
                                     }();
             const float nxt = e_lb * r_lb;
-            if (nxt >= e_floor) {
+            // warp-uniform branch (no convergence barrier): in the rare clamp
+            // round every lane clamps -- a no-op where e >= nxt >= e_floor
+            const bool fine = nxt >= e_floor;
+            if (__all_sync(0xffffffffu, fine)) {
                 e_lb = nxt;
             } else {
 #pragma unroll
@@ -535,7 +543,7 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                         eA[h][n] = floor2(eA[h][n], e_floor);
                         eB[h][n] = floor2(eB[h][n], e_floor);
                     }
-                e_lb = e_floor;
+                e_lb = fine ? nxt : e_floor;
             }
         }
 #endif
