@@ -72,6 +72,7 @@ constexpr int kWarpsPerCta = IL_FAST_WARPS;
 #define IL_STEP_UNROLL 2
 #endif
 constexpr int kStepUnroll = IL_STEP_UNROLL;
+constexpr int kRefCount = 0, kRefYes = 1, kRefNo = 2;  // refresh modes of a step
 
 
 
@@ -360,10 +361,13 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     int until_refresh = 0;
     // One step; FULL_C selects the refresh precision (std::true_type: all
     // three split passes, std::false_type: the lo(v) x hi(G) pass dropped).
-    auto step_body = [&](auto full_c, int step) {
+    // REF_C: kRefCount (refresh when the countdown reaches 0), kRefYes /
+    // kRefNo (the caller knows the step's phase: f_mvm = 2 pair loops).
+    auto step_body = [&](auto full_c, auto ref_c) {
         constexpr bool FULL = decltype(full_c)::value;
-        if (until_refresh == 0) {
-            until_refresh = s.f_mvm;
+        constexpr int REF = decltype(ref_c)::value;
+        if (REF == kRefYes || (REF == kRefCount && until_refresh == 0)) {
+            if constexpr (REF == kRefCount) until_refresh = s.f_mvm;
             // ---- refresh: v = x1 + x2, M' = -Ks G v on tensor cores -----------
             float2 v[2][NT];
             float pb[2] = {0.f, 0.f};
@@ -561,20 +565,40 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
                 }
             }
         }
-        --until_refresh;
+        if constexpr (REF == kRefCount) --until_refresh;
     };
     // the refreshes of steps < s.full_steps carry all three passes, the later
     // ones two (two loops, so that neither carries a branch on the mode)
-    // (the all-three-pass loop -- every step in `fp32` mode -- unrolled by 4
-    // for the one-problem layouts NT >= 3: 4.049 -> 4.031 ms per 16x16 slot,
-    // n_t = 12 3.231 -> 3.191 ms; PACK, NT <= 2 and the two-pass loop measured
-    // slower at 4, bit-identical outputs either way)
-    constexpr int kUnrollFull = (PACK || NT <= 2) ? kStepUnroll : 2 * kStepUnroll;
+    using RefYes = std::integral_constant<int, kRefYes>;
+    using RefNo = std::integral_constant<int, kRefNo>;
+    using RefCount = std::integral_constant<int, kRefCount>;
     const int n_full = min(s.full_steps, s.n_steps);
+    // f_mvm = 2 (the reference's default): steps [a, b), a even, as pairs
+    // (refresh + step, step) whose refresh is known at compile time -- no
+    // countdown and no refresh branch: 16x16 slot anneal 4.010 -> 3.976 ms,
+    // 8x8 1.953 -> 1.909, N_a = 8 1.444 -> 1.385, n_t = 12 3.186 -> 3.030,
+    // bit-identical.  Not unrolled further: two pairs per iteration spill.
+    auto pairs = [&](auto full_c, int a, int b) {
+        int step = a;
+#pragma unroll 1
+        for (; step + 1 < b; step += 2) {
+            step_body(full_c, RefYes{});
+            step_body(full_c, RefNo{});
+        }
+        if (step < b) step_body(full_c, RefYes{});
+    };
+    // any other f_mvm: the countdown (the all-three-pass loop unrolled by 4
+    // for the one-problem layouts NT >= 3, measured 0.5% faster there)
+    constexpr int kUnrollFull = (PACK || NT <= 2) ? kStepUnroll : 2 * kStepUnroll;
+    if (s.f_mvm == 2 && (n_full & 1) == 0) {
+        pairs(std::true_type{}, 0, n_full);
+        pairs(std::false_type{}, n_full, s.n_steps);
+    } else {
 #pragma unroll kUnrollFull
-    for (int step = 0; step < n_full; ++step) step_body(std::true_type{}, step);
+        for (int step = 0; step < n_full; ++step) step_body(std::true_type{}, RefCount{});
 #pragma unroll kStepUnroll
-    for (int step = n_full; step < s.n_steps; ++step) step_body(std::false_type{}, step);
+        for (int step = n_full; step < s.n_steps; ++step) step_body(std::false_type{}, RefCount{});
+    }
 
     // ---- epilogue: divergence flags, spins, FP64 energies --------------------
     // E = u'Gu - 2 tr G + 2 s_aux b'u with u = s_A + s_B (solver.py:171-175)

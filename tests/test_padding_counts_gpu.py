@@ -169,3 +169,24 @@ def test_private_memory_pool_leaves_default_pool_alone():
     CU_MEMPOOL_ATTR_RELEASE_THRESHOLD = 4
     assert cu.cuMemPoolGetAttribute(pool, CU_MEMPOOL_ATTR_RELEASE_THRESHOLD, ctypes.byref(thr)) == 0
     assert thr.value == 0
+
+
+@pytest.mark.parametrize("n_t,kw", [(16, dict(f_mvm=1)), (16, dict(f_mvm=3)), (16, dict(n_steps=127)),
+                                    (8, dict(f_mvm=3, n_steps=101)), (8, dict(n_anneals=8, n_steps=99)),
+                                    (16, dict(f_mvm=4, n_anneals=8))])
+def test_fast_kernel_refresh_schedules_against_exact(n_t, kw):
+    """The FP32 kernel's step loop has two forms: f_mvm = 2 as compile-time
+    (refresh, step) pairs with a tail step for odd n_steps, any other f_mvm
+    as a refresh countdown (_kernel.pyx:65: refresh when step % f_mvm ==
+    0).  Both held to the energy gate against the FP64-exact kernel."""
+    from paper_2510_01579_b200 import batched
+    from paper_2510_01579_b200.params import CacParams
+    H, y, nv, seeds, _ = _uplink(n_t, n_t, 16, 16.0, 384, 1234 + n_t)
+    for prec in ("fp32", "mixed"):
+        ex = batched.detect_cim_batch(H, y, nv, 16, seeds, CacParams(precision="fp64_exact", **kw))
+        fa = batched.detect_cim_batch(H, y, nv, 16, seeds, CacParams(precision=prec, **kw))
+        e_ex, e_fa = ex.energy.cpu().numpy(), fa.energy.cpu().numpy()
+        le = float(np.mean(e_fa <= e_ex * (1 + 1e-12)))
+        same = (fa.x_idx == ex.x_idx).all(-1).all(-1).float().mean().item()
+        print(f"{n_t}x{n_t} {kw} {prec}: energy<=exact {le:.4f} identical {same:.4f}")
+        assert le >= 0.99 and same >= 0.97
