@@ -73,6 +73,9 @@ constexpr int kWarpsPerCta = IL_FAST_WARPS;
 #endif
 constexpr int kStepUnroll = IL_STEP_UNROLL;
 constexpr int kRefCount = 0, kRefYes = 1, kRefNo = 2;  // refresh modes of a step
+#ifndef IL_PAIRS_NT_MASK  // register layouts NT (bit NT) whose f_mvm = 2 loop runs as step pairs
+#define IL_PAIRS_NT_MASK 0x1FE  // every layout NT = 1-8 (tools/gpu/ab_large_nt.sh)
+#endif
 
 
 
@@ -577,7 +580,9 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     // (refresh + step, step) whose refresh is known at compile time -- no
     // countdown and no refresh branch: 16x16 slot anneal 4.010 -> 3.976 ms,
     // 8x8 1.953 -> 1.909, N_a = 8 1.444 -> 1.385, n_t = 12 3.186 -> 3.030,
-    // bit-identical.  Not unrolled further: two pairs per iteration spill.
+    // n_t = 20 / 24 / 28 / 32 6.24 / 7.34 / 9.82 / 12.79 -> 6.02 / 7.20 /
+    // 9.32 / 10.87, bit-identical.  Not unrolled further: two pairs per
+    // iteration spill.
     auto pairs = [&](auto full_c, int a, int b) {
         int step = a;
 #pragma unroll 1
@@ -588,9 +593,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
         if (step < b) step_body(full_c, RefYes{});
     };
     // any other f_mvm: the countdown (the all-three-pass loop unrolled by 4
-    // for the one-problem layouts NT >= 3, measured 0.5% faster there)
-    constexpr int kUnrollFull = (PACK || NT <= 2) ? kStepUnroll : 2 * kStepUnroll;
-    if (s.f_mvm == 2 && (n_full & 1) == 0) {
+    // for the one-problem layouts NT = 3, 4: 0.5% faster there; at NT >= 5
+    // the unrolled countdown also slowed the pairs loop beside it: n_t = 20
+    // anneal 6.60 vs 6.02 ms)
+    constexpr int kUnrollFull = (PACK || NT <= 2 || NT >= 5) ? kStepUnroll : 2 * kStepUnroll;
+    constexpr bool kPairs = (IL_PAIRS_NT_MASK >> NT) & 1;
+    if (kPairs && s.f_mvm == 2 && (n_full & 1) == 0) {
         pairs(std::true_type{}, 0, n_full);
         pairs(std::false_type{}, n_full, s.n_steps);
     } else {
