@@ -76,6 +76,9 @@ constexpr int kRefCount = 0, kRefYes = 1, kRefNo = 2;  // refresh modes of a ste
 #ifndef IL_PAIRS_NT_MASK  // register layouts NT (bit NT) whose f_mvm = 2 loop runs as step pairs
 #define IL_PAIRS_NT_MASK 0x1FE  // every layout NT = 1-8 (tools/gpu/ab_large_nt.sh)
 #endif
+#ifndef IL_PAIR_UNROLL2_MAX_NT  // layouts NT <= this run two step pairs per loop iteration
+#define IL_PAIR_UNROLL2_MAX_NT 2  // 8x8 anneal 1.904 -> 1.882 ms; NT = 3, 4 spill at 2
+#endif
 
 
 
@@ -581,11 +584,12 @@ k_anneal_fast(const double* __restrict__ Gall, const double* __restrict__ gall,
     // countdown and no refresh branch: 16x16 slot anneal 4.010 -> 3.976 ms,
     // 8x8 1.953 -> 1.909, N_a = 8 1.444 -> 1.385, n_t = 12 3.186 -> 3.030,
     // n_t = 20 / 24 / 28 / 32 6.24 / 7.34 / 9.82 / 12.79 -> 6.02 / 7.20 /
-    // 9.32 / 10.87, bit-identical.  Not unrolled further: two pairs per
-    // iteration spill.
+    // 9.32 / 10.87, bit-identical.  Two pairs per iteration only for NT <= 2
+    // (8x8 anneal 1.904 -> 1.882 ms); for NT >= 3 they spill.
+    constexpr int kPairUnroll = NT <= IL_PAIR_UNROLL2_MAX_NT ? 2 : 1;
     auto pairs = [&](auto full_c, int a, int b) {
         int step = a;
-#pragma unroll 1
+#pragma unroll kPairUnroll
         for (; step + 1 < b; step += 2) {
             step_body(full_c, RefYes{});
             step_body(full_c, RefNo{});
